@@ -1,0 +1,218 @@
+// encode.cu — K6 (prefill sign-hash encode), K5 (per-step append), helpers.
+#include "encode.cuh"
+
+namespace clo {
+
+namespace {
+
+constexpr int kEncRows = 32;
+constexpr int kEncThreads = 256;
+
+// One CTA = 32 rows of one segment x all bits. Rows are widened to double in
+// shared memory; thread b walks c = 0..d-1 once, keeping 32 sequential row
+// accumulators (P[b][c] read once per c, coalesced from P^T).
+template <typename T>
+__global__ void __launch_bounds__(kEncThreads) encode_kernel(const EncodeSeg* segs, int64_t n,
+                                                             int d, int bits, int* err) {
+    extern __shared__ double ks[];  // [kEncRows][d]
+    const EncodeSeg sg = segs[blockIdx.y];
+    const int words = (bits + 63) / 64;
+    const int64_t r0 = (int64_t)blockIdx.x * kEncRows;
+    const int nr = (int)(n - r0 < kEncRows ? n - r0 : kEncRows);
+    const T* rows = static_cast<const T*>(sg.rows) + r0 * d;
+    for (int i = threadIdx.x; i < nr * d; i += blockDim.x) {
+        const double x = to_f64<T>(rows[i]);
+        if (!isfinite(x)) raise_err(err, kErrNonFiniteKey);
+        ks[i] = x;
+    }
+    __syncthreads();
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(sg.codes + r0 * words);
+    for (int b0 = 0; b0 < words * 64; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        double s[kEncRows];
+#pragma unroll
+        for (int r = 0; r < kEncRows; ++r) s[r] = 0.0;
+        if (b < bits) {
+            for (int c = 0; c < d; ++c) {
+                const double p = sg.proj_t[(size_t)c * bits + b];
+#pragma unroll
+                for (int r = 0; r < kEncRows; ++r) s[r] = dmac(s[r], p, ks[r * d + c]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kEncRows; ++r) {
+            const unsigned bal = __ballot_sync(0xffffffffu, b < bits && s[r] >= 0.0);
+            if ((threadIdx.x & 31) == 0 && r < nr && b < words * 64)
+                out32[(size_t)r * words * 2 + (b >> 5)] = bal;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_row(void* base, size_t row, int d, const T* src) {
+    T* dst = static_cast<T*>(base) + row * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
+}
+
+// One CTA per (sequence, KV head) of one layer.
+template <typename T>
+__global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l) {
+    const int b = blockIdx.x / v.H, g = blockIdx.x % v.H;
+    const int lg = l * v.H + g;
+    const int seg = (b * v.L + l) * v.H + g;
+    const bool pers = v.persistent[lg] != 0;
+    const int t = *v.dev_step + 1;
+    const int row = v.n_prompt + t - 1;  // n_pool: the new token's index
+    __shared__ T kr[kMaxHeadDim], vr[kMaxHeadDim];
+    __shared__ double kd[kMaxHeadDim];
+    const size_t off = (((size_t)b * v.L + l) * v.H + g) * v.d;
+    const T* nk = static_cast<const T*>(v.desc->new_k) + off;
+    const T* nv = static_cast<const T*>(v.desc->new_v) + off;
+    for (int i = threadIdx.x; i < v.d; i += blockDim.x) {
+        kr[i] = nk[i];
+        vr[i] = nv[i];
+        const double x = to_f64<T>(kr[i]);
+        if (!isfinite(x)) raise_err(v.err, kErrNonFiniteKey);
+        if (!isfinite(to_f64<T>(vr[i]))) raise_err(v.err, kErrNonFiniteValue);
+        kd[i] = x;
+    }
+    __syncthreads();
+    if (pers) {
+        const size_t p = (size_t)b * v.NP + v.pidx[lg];
+        store_row<T>(v.pk, p * v.nmax + row, v.d, kr);
+        store_row<T>(v.pv, p * v.nmax + row, v.d, vr);
+    } else {
+        const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+        T* hk = static_cast<T*>(v.host_k_w) + hb;
+        T* hv = static_cast<T*>(v.host_v_w) + hb;
+        store_row<T>(hk, row, v.d, kr);  // zero-copy store into the pinned host store
+        store_row<T>(hv, row, v.d, vr);
+        const size_t o = (size_t)b * v.NO + v.oidx[lg];
+        const int wrows = v.sink + v.recent;
+        if (row < v.sink) {
+            store_row<T>(v.win_k, o * wrows + row, v.d, kr);
+            store_row<T>(v.win_v, o * wrows + row, v.d, vr);
+        }
+        if (v.recent > 0) {
+            store_row<T>(v.win_k, o * wrows + v.sink + row % v.recent, v.d, kr);
+            store_row<T>(v.win_v, o * wrows + v.sink + row % v.recent, v.d, vr);
+        }
+        if (v.kmirror) store_row<T>(v.kmirror, o * v.nmax + row, v.d, kr);
+    }
+    if (v.retriever == 1) {
+        uint32_t* out32 = reinterpret_cast<uint32_t*>(v.codes + ((size_t)seg * v.nmax + row) * v.words);
+        const double* pt = v.proj_t + (size_t)lg * v.d * v.bits;
+        for (int b0 = 0; b0 < v.words * 64; b0 += blockDim.x) {
+            const int bit = b0 + threadIdx.x;
+            double s = 0.0;
+            if (bit < v.bits)
+                for (int c = 0; c < v.d; ++c) s = dmac(s, pt[(size_t)c * v.bits + bit], kd[c]);
+            const unsigned bal = __ballot_sync(0xffffffffu, bit < v.bits && s >= 0.0);
+            if ((threadIdx.x & 31) == 0 && bit < v.words * 64) out32[bit >> 5] = bal;
+        }
+    }
+}
+
+__global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L) {
+    if (threadIdx.x == 0) *dev_step += 1;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        ca[i] = 0;
+        cb[i] = 0;
+    }
+}
+
+template <typename T>
+__global__ void check_finite_kernel(const T* p, int64_t count, int* err, int bit) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(to_f64<T>(p[i]));
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, bit);
+}
+
+template <typename T>
+__global__ void window_init_kernel(EngineView v) {
+    const int seg = blockIdx.x;
+    const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+    const int lg = l * v.H + g;
+    if (v.persistent[lg]) return;
+    const size_t o = (size_t)b * v.NO + v.oidx[lg];
+    const int n = v.n_prompt, wrows = v.sink + v.recent;
+    const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+    const T* hk = static_cast<const T*>(v.host_k) + hb;
+    const T* hv = static_cast<const T*>(v.host_v) + hb;
+    T* wk = static_cast<T*>(v.win_k) + o * wrows * v.d;
+    T* wv = static_cast<T*>(v.win_v) + o * wrows * v.d;
+    const int ns = min(v.sink, n);
+    for (int i = threadIdx.x; i < ns * v.d; i += blockDim.x) {
+        wk[i] = hk[i];
+        wv[i] = hv[i];
+    }
+    if (v.recent > 0) {
+        const int t0 = max(0, n - v.recent);
+        for (int i = threadIdx.x; i < (n - t0) * v.d; i += blockDim.x) {
+            const int t = t0 + i / v.d, c = i % v.d;
+            const size_t dst = (size_t)(v.sink + t % v.recent) * v.d + c;
+            wk[dst] = hk[(size_t)t * v.d + c];
+            wv[dst] = hv[(size_t)t * v.d + c];
+        }
+    }
+}
+
+}  // namespace
+
+void launch_encode(const EncodeSeg* segs_dev, int n_segs, int64_t n, int d, int bits, int dtype,
+                   int* err, cudaStream_t stream) {
+    if (n <= 0 || n_segs <= 0) return;
+    dim3 grid((unsigned)((n + kEncRows - 1) / kEncRows), (unsigned)n_segs);
+    const size_t sm = (size_t)kEncRows * d * sizeof(double);
+    switch (dtype) {
+        case kBF16:
+            encode_kernel<__nv_bfloat16><<<grid, kEncThreads, sm, stream>>>(segs_dev, n, d, bits, err);
+            break;
+        case kF32:
+            encode_kernel<float><<<grid, kEncThreads, sm, stream>>>(segs_dev, n, d, bits, err);
+            break;
+        default:
+            encode_kernel<double><<<grid, kEncThreads, sm, stream>>>(segs_dev, n, d, bits, err);
+            break;
+    }
+}
+
+void launch_append(const EngineView& v, int layer, cudaStream_t stream) {
+    if (v.kv_dtype == kBF16)
+        append_kernel<__nv_bfloat16><<<v.B * v.H, kEncThreads, 0, stream>>>(v, layer);
+    else
+        append_kernel<float><<<v.B * v.H, kEncThreads, 0, stream>>>(v, layer);
+}
+
+void launch_step_end(const EngineView& v, int* count_a, int* count_b, cudaStream_t stream) {
+    step_end_kernel<<<1, 128, 0, stream>>>(v.dev_step, count_a, count_b, v.L);
+}
+
+void launch_check_finite(const void* p, int dtype, int64_t count, int* err, int bit,
+                         cudaStream_t stream) {
+    if (count <= 0) return;
+    int64_t blocks = (count + 255) / 256;
+    const int grid = (int)(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16);
+    switch (dtype) {
+        case kBF16:
+            check_finite_kernel<<<grid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(p), count, err, bit);
+            break;
+        case kF32:
+            check_finite_kernel<<<grid, 256, 0, stream>>>(static_cast<const float*>(p), count, err, bit);
+            break;
+        default:
+            check_finite_kernel<<<grid, 256, 0, stream>>>(static_cast<const double*>(p), count, err, bit);
+            break;
+    }
+}
+
+void launch_window_init(const EngineView& v, cudaStream_t stream) {
+    if (v.kv_dtype == kBF16)
+        window_init_kernel<__nv_bfloat16><<<v.B * v.L * v.H, 256, 0, stream>>>(v);
+    else
+        window_init_kernel<float><<<v.B * v.L * v.H, 256, 0, stream>>>(v);
+}
+
+}  // namespace clo

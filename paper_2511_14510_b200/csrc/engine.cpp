@@ -1,0 +1,790 @@
+// engine.cpp — host side of the B200 DecodeEngine (engine.hpp:91-139,
+// engine.cpp:106-557 of the reference). The host validates, allocates,
+// uploads profiles/projections, and records ONE CUDA graph per decode step;
+// every per-step decision (hit/miss, selection, transfer, append, attention)
+// happens on the device.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <vector>
+
+#include "attention.cuh"
+#include "encode.cuh"
+#include "gather.cuh"
+#include "lookup.cuh"
+#include "select.cuh"
+
+namespace clo {
+
+namespace {
+
+int grid_for(int64_t units) {
+    const int64_t cap = (int64_t)kNumSMs * 8;
+    if (units < 1) return 1;
+    return (int)std::min<int64_t>(units, cap);
+}
+
+}  // namespace
+
+Engine::Engine(const clo_engine_config& cfg, const double* tau, const double* q_importance,
+               const int* persistent)
+    : cfg_(cfg) {
+    const clo_model_shape& s = cfg.shape;
+    // ModelShape::validate (matrix.hpp:57-65)
+    if (s.num_layers <= 0) fail(CLO_ERR_CONFIG, "num_layers must be positive");
+    if (s.num_q_heads <= 0 || s.num_kv_heads <= 0) fail(CLO_ERR_CONFIG, "head counts must be positive");
+    if (s.num_q_heads % s.num_kv_heads != 0)
+        fail(CLO_ERR_CONFIG, "num_q_heads must be a multiple of num_kv_heads");
+    if (s.head_dim <= 0) fail(CLO_ERR_CONFIG, "head_dim must be positive");
+    if (s.bytes_per_element <= 0) fail(CLO_ERR_CONFIG, "bytes_per_element must be positive");
+    // DecodeEngine ctor checks (engine.cpp:115-136)
+    if (cfg.k < 1) fail(CLO_ERR_ARGUMENT, "k must be at least 1");
+    if (cfg.k > cfg.n_prompt) fail(CLO_ERR_ARGUMENT, "k exceeds the prompt length; nothing to select from at step 0");
+    if (cfg.sink_tokens < 0 || cfg.recent_tokens < 0) fail(CLO_ERR_ARGUMENT, "window sizes must be non-negative");
+    if (cfg.policy == CLO_POLICY_LRU || cfg.policy == CLO_POLICY_LFU)
+        fail(CLO_ERR_CONFIG, "block-cache policies (lru/lfu) are outside the CLO hot path");
+    if (cfg.policy != CLO_POLICY_SIMILARITY && cfg.policy != CLO_POLICY_PREFETCH_ONLY)
+        fail(CLO_ERR_CONFIG, "unknown policy");
+    if (cfg.always_hit && cfg.always_miss) fail(CLO_ERR_CONFIG, "always_hit and always_miss are mutually exclusive");
+    if (cfg.compute_oracle_error)
+        fail(CLO_ERR_CONFIG, "compute_oracle_error is a CPU-oracle metric; run the oracle in tests instead");
+    if (cfg.retriever != CLO_RETRIEVER_EXACT && cfg.retriever != CLO_RETRIEVER_SIGN_HASH)
+        fail(CLO_ERR_CONFIG, "unknown retriever");
+    if (cfg.retriever == CLO_RETRIEVER_SIGN_HASH && (cfg.hash_bits <= 0 || cfg.hash_bits % 8 != 0))
+        fail(CLO_ERR_ARGUMENT, "hash_bits must be a positive multiple of 8");
+    if (cfg.hash_bits > 64 * kMaxHashWords) fail(CLO_ERR_CONFIG, "hash_bits above 512 are not supported");
+    if (cfg.batch < 1) fail(CLO_ERR_CONFIG, "batch must be positive");
+    if (cfg.max_steps < 0) fail(CLO_ERR_CONFIG, "max_steps must be non-negative");
+    if (cfg.kv_dtype != CLO_DTYPE_BF16 && cfg.kv_dtype != CLO_DTYPE_F32)
+        fail(CLO_ERR_CONFIG, "kv_dtype must be BF16 or F32");
+    const int m = s.num_q_heads / s.num_kv_heads;
+    if (m > kMaxGroup) fail(CLO_ERR_CONFIG, "GQA group size above 16 is not supported");
+    if (!attention_supported(cfg.kv_dtype, s.head_dim, m))
+        fail(CLO_ERR_CONFIG, "head_dim must be one of 8/16/32/64/128/256 and the GQA group <= 8");
+    if ((s.head_dim * (cfg.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4)) % 16 != 0)
+        fail(CLO_ERR_CONFIG, "K/V rows must be a multiple of 16 bytes");
+    if (cfg.sink_tokens + cfg.recent_tokens > 4096) fail(CLO_ERR_CONFIG, "window too large");
+
+    const int L = s.num_layers, H = s.num_kv_heads;
+    tau_.assign(tau, tau + (size_t)L * H);
+    qimp_.assign(q_importance, q_importance + (size_t)L * H * m);
+    for (double w : qimp_)
+        if (w < 0.0) fail(CLO_ERR_ARGUMENT, "importance weights must be non-negative");
+    persistent_.resize((size_t)L * H);
+    pidx_.assign((size_t)L * H, -1);
+    oidx_.assign((size_t)L * H, -1);
+    for (int i = 0; i < L * H; ++i) {
+        persistent_[i] = persistent[i] ? 1 : 0;
+        if (persistent_[i])
+            pidx_[i] = np_++;
+        else
+            oidx_[i] = no_++;
+    }
+    layer_has_pers_.assign(L, 0);
+    layer_has_off_.assign(L, 0);
+    for (int l = 0; l < L; ++l)
+        for (int g = 0; g < H; ++g) (persistent_[l * H + g] ? layer_has_pers_ : layer_has_off_)[l] = 1;
+
+    sync_mode_ = cfg.sync_override >= 0 ? cfg.sync_override
+                                        : (cfg.policy == CLO_POLICY_SIMILARITY ? CLO_SYNC_GPU_CENTRIC
+                                                                               : CLO_SYNC_CPU_CENTRIC);
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        fail(CLO_ERR_CUDA, "no CUDA device: the CLO path has no CPU fallback");
+    CLO_CUDA(cudaSetDevice(cfg.device));
+    allocate();
+}
+
+Engine::~Engine() {
+    cudaSetDevice(cfg_.device);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    for (auto ev : ev_attn_) cudaEventDestroy(ev);
+    for (auto ev : ev_pref_) cudaEventDestroy(ev);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (s_main_) cudaStreamDestroy(s_main_);
+    if (s_pref_) cudaStreamDestroy(s_pref_);
+    if (desc_host_) cudaFreeHost(desc_host_);
+    for (auto ev : desc_ev_) cudaEventDestroy(ev);
+}
+
+void Engine::allocate() {
+    const clo_model_shape& s = cfg_.shape;
+    const int B = cfg_.batch, L = s.num_layers, H = s.num_kv_heads, HQ = s.num_q_heads;
+    const int m = HQ / H, d = s.head_dim, k = cfg_.k;
+    const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    nmax_ = cfg_.n_prompt + cfg_.max_steps;
+    max_chunks_ = (nmax_ + kScoreChunk - 1) / kScoreChunk;
+    words_ = (cfg_.hash_bits + 63) / 64;
+    nb_ = cfg_.hash_bits + 1;
+    const size_t segs = (size_t)B * L * H;
+    const size_t wrows = (size_t)cfg_.sink_tokens + cfg_.recent_tokens;
+
+    d_persistent_.alloc(sizeof(int) * L * H);
+    d_pidx_.alloc(sizeof(int) * L * H);
+    d_oidx_.alloc(sizeof(int) * L * H);
+    CLO_CUDA(cudaMemcpy(d_persistent_.p, persistent_.data(), sizeof(int) * L * H, cudaMemcpyHostToDevice));
+    CLO_CUDA(cudaMemcpy(d_pidx_.p, pidx_.data(), sizeof(int) * L * H, cudaMemcpyHostToDevice));
+    CLO_CUDA(cudaMemcpy(d_oidx_.p, oidx_.data(), sizeof(int) * L * H, cudaMemcpyHostToDevice));
+    d_tau_.alloc(sizeof(double) * L * H);
+    d_qimp_.alloc(sizeof(double) * L * H * m);
+    CLO_CUDA(cudaMemcpy(d_tau_.p, tau_.data(), sizeof(double) * L * H, cudaMemcpyHostToDevice));
+    CLO_CUDA(cudaMemcpy(d_qimp_.p, qimp_.data(), sizeof(double) * L * H * m, cudaMemcpyHostToDevice));
+
+    d_pk_.alloc((size_t)B * np_ * nmax_ * d * esz, false);
+    d_pv_.alloc((size_t)B * np_ * nmax_ * d * esz, false);
+    if (cfg_.retriever == CLO_RETRIEVER_EXACT) d_kmirror_.alloc((size_t)B * no_ * nmax_ * d * esz, false);
+    d_slot_k_.alloc((size_t)B * no_ * k * d * esz);
+    d_slot_v_.alloc((size_t)B * no_ * k * d * esz);
+    d_win_k_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
+    d_win_v_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
+    d_entry_idx_.alloc(sizeof(int32_t) * segs * k);
+    if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
+        d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_, false);
+        // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
+        // (engine.cpp:172-174); stored transposed [d][bits] for coalesced reads.
+        std::vector<double> pt((size_t)L * H * d * cfg_.hash_bits);
+        std::vector<double> p((size_t)cfg_.hash_bits * d);
+        for (int l = 0; l < L; ++l)
+            for (int g = 0; g < H; ++g) {
+                const uint64_t seed = mix_seed3(cfg_.retriever_seed, (uint64_t)l,
+                                                (uint64_t)(g + cfg_.kv_head_offset));
+                sign_hash_projection(cfg_.hash_bits, d, seed, p.data());
+                double* dst = pt.data() + ((size_t)l * H + g) * d * cfg_.hash_bits;
+                for (int b = 0; b < cfg_.hash_bits; ++b)
+                    for (int c = 0; c < d; ++c) dst[(size_t)c * cfg_.hash_bits + b] = p[(size_t)b * d + c];
+            }
+        d_proj_t_.alloc(sizeof(double) * pt.size(), false);
+        CLO_CUDA(cudaMemcpy(d_proj_t_.p, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice));
+    }
+    d_labels_.alloc(sizeof(double) * B * L * HQ * d);
+    d_label_valid_.alloc(sizeof(int) * B * L * HQ);
+    d_hits_.alloc(sizeof(unsigned long long) * segs);
+    d_misses_.alloc(sizeof(unsigned long long) * segs);
+    d_cache_last_.alloc(sizeof(int) * segs);
+    d_entry_last_.alloc(sizeof(int) * segs);
+    d_last_hit_.alloc(sizeof(int) * segs);
+    {
+        std::vector<int> minus1(segs, -1);
+        CLO_CUDA(cudaMemcpy(d_cache_last_.p, minus1.data(), sizeof(int) * segs, cudaMemcpyHostToDevice));
+        CLO_CUDA(cudaMemcpy(d_entry_last_.p, minus1.data(), sizeof(int) * segs, cudaMemcpyHostToDevice));
+    }
+    d_history_.alloc(sizeof(double) * segs * std::max(cfg_.max_steps, 1));
+    d_gathered_.alloc(sizeof(unsigned long long));
+    d_step_.alloc(sizeof(int));
+    d_desc_.alloc(sizeof(StepDesc));
+    d_err_.alloc(sizeof(int));
+    max_attn_chunks_ = attention_chunks(k, cfg_.sink_tokens, cfg_.recent_tokens);
+    d_attn_part_.alloc(sizeof(float) * B * H * max_attn_chunks_ * m * (d + 2), false);
+    d_attn_count_.alloc(sizeof(int) * B * H);
+
+    // staging for host-resident step inputs / outputs
+    d_in_tq_.alloc(sizeof(float) * B * L * HQ * d, false);
+    d_in_aq_.alloc(sizeof(float) * B * L * HQ * d, false);
+    d_in_nk_.alloc(esz * B * L * H * d, false);
+    d_in_nv_.alloc(esz * B * L * H * d, false);
+    d_out_.alloc(sizeof(float) * B * L * HQ * d, false);
+
+    for (int i = 0; i < 2; ++i) {
+        SelScratch& sc = scratch_[i];
+        auto& bufs = scratch_bufs_[i];
+        const size_t items = (size_t)B * H;
+        bufs[0].alloc(sizeof(int) * L);
+        bufs[1].alloc(sizeof(SelItem) * items);
+        bufs[2].alloc(sizeof(double) * items * m * d);
+        bufs[3].alloc(sizeof(uint64_t) * items * m * words_);
+        if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH)
+            bufs[4].alloc(sizeof(uint16_t) * items * nmax_, false);
+        else
+            bufs[5].alloc(sizeof(uint64_t) * items * nmax_, false);
+        bufs[6].alloc(sizeof(uint32_t) * items * max_chunks_ * std::max(nb_, 2), false);
+        bufs[7].alloc(sizeof(int) * items * max_chunks_);
+        bufs[8].alloc(sizeof(int) * items * max_chunks_);
+        bufs[9].alloc(sizeof(uint64_t) * items);
+        bufs[10].alloc(sizeof(int) * items);
+        bufs[11].alloc(sizeof(uint32_t) * items * 256);
+        sc.count = bufs[0].as<int>();
+        sc.items = bufs[1].as<SelItem>();
+        sc.q64 = bufs[2].as<double>();
+        sc.qbits = bufs[3].as<uint64_t>();
+        sc.key16 = bufs[4].as<uint16_t>();
+        sc.key64 = bufs[5].as<uint64_t>();
+        sc.chunk_hist = bufs[6].as<uint32_t>();
+        sc.chunk_base = bufs[7].as<int>();
+        sc.chunk_take = bufs[8].as<int>();
+        sc.thresh = bufs[9].as<uint64_t>();
+        sc.need = bufs[10].as<int>();
+        sc.radix_hist = bufs[11].as<uint32_t>();
+    }
+
+    CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
+    CLO_CUDA(cudaStreamCreateWithFlags(&s_pref_, cudaStreamNonBlocking));
+    CLO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    CLO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    ev_attn_.resize(L);
+    ev_pref_.resize(L);
+    for (int l = 0; l < L; ++l) {
+        CLO_CUDA(cudaEventCreateWithFlags(&ev_attn_[l], cudaEventDisableTiming));
+        CLO_CUDA(cudaEventCreateWithFlags(&ev_pref_[l], cudaEventDisableTiming));
+    }
+    CLO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&desc_host_), sizeof(StepDesc) * kDescRing,
+                           cudaHostAllocDefault));
+    desc_ev_.resize(kDescRing);
+    for (auto& ev : desc_ev_) CLO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    desc_used_.assign(kDescRing, 0);
+    CLO_CUDA(cudaDeviceSynchronize());
+}
+
+EngineView Engine::view() const {
+    const clo_model_shape& s = cfg_.shape;
+    EngineView v{};
+    v.B = cfg_.batch;
+    v.L = s.num_layers;
+    v.H = s.num_kv_heads;
+    v.HQ = s.num_q_heads;
+    v.m = v.HQ / v.H;
+    v.d = s.head_dim;
+    v.k = cfg_.k;
+    v.sink = cfg_.sink_tokens;
+    v.recent = cfg_.recent_tokens;
+    v.bits = cfg_.hash_bits;
+    v.words = words_;
+    v.nb = nb_;
+    v.n_prompt = cfg_.n_prompt;
+    v.nmax = nmax_;
+    v.max_steps = std::max(cfg_.max_steps, 1);
+    v.max_chunks = max_chunks_;
+    v.retriever = cfg_.retriever;
+    v.policy = cfg_.policy;
+    v.always_miss = cfg_.always_miss;
+    v.always_hit = cfg_.always_hit;
+    v.has_tau_override = cfg_.has_tau_override;
+    v.tau_override = cfg_.tau_override;
+    v.kv_dtype = cfg_.kv_dtype;
+    v.NP = np_;
+    v.NO = no_;
+    v.host_k = host_k_;
+    v.host_v = host_v_;
+    v.host_k_w = host_k_;
+    v.host_v_w = host_v_;
+    v.seq_stride = seq_stride_;
+    v.layer_stride = layer_stride_;
+    v.head_stride = head_stride_;
+    v.persistent = d_persistent_.as<int>();
+    v.pidx = d_pidx_.as<int>();
+    v.oidx = d_oidx_.as<int>();
+    v.pk = d_pk_.p;
+    v.pv = d_pv_.p;
+    v.kmirror = d_kmirror_.p;
+    v.slot_k = d_slot_k_.p;
+    v.slot_v = d_slot_v_.p;
+    v.win_k = d_win_k_.p;
+    v.win_v = d_win_v_.p;
+    v.entry_idx = d_entry_idx_.as<int32_t>();
+    v.codes = d_codes_.as<uint64_t>();
+    v.proj_t = d_proj_t_.as<double>();
+    v.labels = d_labels_.as<double>();
+    v.label_valid = d_label_valid_.as<int>();
+    v.tau = d_tau_.as<double>();
+    v.qimp = d_qimp_.as<double>();
+    v.hits = d_hits_.as<unsigned long long>();
+    v.misses = d_misses_.as<unsigned long long>();
+    v.cache_last_update = d_cache_last_.as<int>();
+    v.entry_last_update = d_entry_last_.as<int>();
+    v.last_lookup_hit = d_last_hit_.as<int>();
+    v.history = d_history_.as<double>();
+    v.gathered_bytes = d_gathered_.as<unsigned long long>();
+    v.dev_step = d_step_.as<int>();
+    v.desc = d_desc_.as<StepDesc>();
+    v.err = d_err_.as<int>();
+    v.attn_part = d_attn_part_.as<float>();
+    v.attn_count = d_attn_count_.as<int>();
+    v.max_attn_chunks = max_attn_chunks_;
+    return v;
+}
+
+SelArgs Engine::sel_args(int which, int layer) const {
+    const clo_model_shape& s = cfg_.shape;
+    const SelScratch& sc = scratch_[which];
+    SelArgs a{};
+    a.items = sc.items;
+    a.count = sc.count + layer;
+    a.m = s.num_q_heads / s.num_kv_heads;
+    a.d = s.head_dim;
+    a.k = cfg_.k;
+    a.bits = cfg_.hash_bits;
+    a.words = words_;
+    a.nb = nb_;
+    a.nmax = nmax_;
+    a.max_chunks = max_chunks_;
+    a.dtype = cfg_.kv_dtype;
+    a.q64 = sc.q64;
+    a.qbits = sc.qbits;
+    a.key16 = sc.key16;
+    a.key64 = sc.key64;
+    a.chunk_hist = sc.chunk_hist;
+    a.chunk_base = sc.chunk_base;
+    a.chunk_take = sc.chunk_take;
+    a.thresh = sc.thresh;
+    a.need = sc.need;
+    a.radix_hist = sc.radix_hist;
+    a.grid = grid_for((int64_t)cfg_.batch * s.num_kv_heads * max_chunks_);
+    return a;
+}
+
+void Engine::enqueue_select(int which, int layer, cudaStream_t st) {
+    SelArgs a = sel_args(which, layer);
+    if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
+        launch_select_signhash(a, st);
+        launches_ += 3;
+    } else {
+        launch_select_exact(a, st);
+        launches_ += 21;
+    }
+}
+
+void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st) {
+    PrepareArgs pa{};
+    pa.v = view();
+    pa.s = scratch_[which];
+    pa.layer = layer;
+    pa.mode = mode;
+    pa.kind = kind;
+    launch_prepare(pa, st);
+    launches_ += 1;
+}
+
+void Engine::enqueue_gather(int which, int layer, int count_bytes, cudaStream_t st) {
+    GatherEngineArgs ga{};
+    ga.v = view();
+    ga.items = scratch_[which].items;
+    ga.count = scratch_[which].count;
+    ga.layer = layer;
+    ga.count_bytes = count_bytes;
+    const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    const int64_t vecs = (int64_t)cfg_.k * cfg_.shape.head_dim * esz / 16;
+    const int64_t units = (int64_t)cfg_.batch * cfg_.shape.num_kv_heads * ((vecs + 1023) / 1024);
+    launch_gather_engine(ga, grid_for(units), st);
+    launches_ += 1;
+}
+
+void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride,
+                          int64_t head_stride) {
+    if (!k || !v) fail(CLO_ERR_ARGUMENT, "host K/V pointers must be non-null");
+    for (void* p : {k, v}) {
+        cudaPointerAttributes at{};
+        CLO_CUDA(cudaPointerGetAttributes(&at, p));
+        if (at.type != cudaMemoryTypeHost)
+            fail(CLO_ERR_ARGUMENT,
+                 "host K/V must be pinned, UVA-mapped memory (clo_host_alloc or cudaHostRegister)");
+    }
+    if (seq_stride < 0 || layer_stride < 0 || head_stride < 0) fail(CLO_ERR_ARGUMENT, "negative stride");
+    host_k_ = k;
+    host_v_ = v;
+    seq_stride_ = seq_stride;
+    layer_stride_ = layer_stride;
+    head_stride_ = head_stride;
+    if (graph_exec_) {  // pointers are baked into the graph
+        cudaGraphExecDestroy(graph_exec_);
+        cudaGraphDestroy(graph_);
+        graph_exec_ = nullptr;
+        graph_ = nullptr;
+    }
+}
+
+void Engine::set_desc(const StepDesc& d, cudaStream_t st) {
+    const int slot = desc_next_;
+    desc_next_ = (desc_next_ + 1) % kDescRing;
+    if (desc_used_[slot]) CLO_CUDA(cudaEventSynchronize(desc_ev_[slot]));
+    desc_host_[slot] = d;
+    CLO_CUDA(cudaMemcpyAsync(d_desc_.p, desc_host_ + slot, sizeof(StepDesc), cudaMemcpyHostToDevice, st));
+    CLO_CUDA(cudaEventRecord(desc_ev_[slot], st));
+    desc_used_[slot] = 1;
+}
+
+void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
+    if (prefilled_) fail(CLO_ERR_CONTRACT, "prefill ran twice");
+    if (!host_k_) fail(CLO_ERR_CONTRACT, "bind the host K/V store before prefill");
+    if (!true_q0) fail(CLO_ERR_ARGUMENT, "true_q0 must be non-null");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    const clo_model_shape& s = cfg_.shape;
+    const int B = cfg_.batch, L = s.num_layers, H = s.num_kv_heads, HQ = s.num_q_heads, d = s.head_dim;
+    const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    const int n = cfg_.n_prompt;
+    cudaStream_t st = s_main_;
+    CLO_CUDA(cudaStreamSynchronize(user));
+
+    // step-0 queries
+    const size_t qbytes = sizeof(float) * B * L * HQ * d;
+    const float* tq = true_q0;
+    if (on_host) {
+        CLO_CUDA(cudaMemcpyAsync(d_in_tq_.p, true_q0, qbytes, cudaMemcpyHostToDevice, st));
+        tq = d_in_tq_.as<float>();
+    }
+    StepDesc desc{tq, tq, nullptr, nullptr, nullptr};
+    set_desc(desc, st);
+    CLO_CUDA(cudaMemsetAsync(d_err_.p, 0, sizeof(int), st));
+
+    // Load prompt rows: stage each distinct host matrix once in HBM, encode its
+    // sign bits for every layer that aliases it, fill persistent KV / K mirror.
+    DevBuf stage_k, stage_v;
+    stage_k.alloc((size_t)n * d * esz, false);
+    stage_v.alloc((size_t)n * d * esz, false);
+    std::vector<EncodeSeg> segs;
+    DevBuf d_segs;
+    d_segs.alloc(sizeof(EncodeSeg) * L);
+    const char* hk = static_cast<const char*>(host_k_);
+    const char* hv = static_cast<const char*>(host_v_);
+    for (int b = 0; b < B; ++b)
+        for (int g = 0; g < H; ++g) {
+            int l0 = 0;
+            while (l0 < L) {
+                const int l1 = layer_stride_ == 0 ? L : l0 + 1;  // layers sharing this host buffer
+                const size_t hoff = ((size_t)b * seq_stride_ + (size_t)l0 * layer_stride_ + (size_t)g * head_stride_) * esz;
+                CLO_CUDA(cudaMemcpyAsync(stage_k.p, hk + hoff, (size_t)n * d * esz, cudaMemcpyHostToDevice, st));
+                CLO_CUDA(cudaMemcpyAsync(stage_v.p, hv + hoff, (size_t)n * d * esz, cudaMemcpyHostToDevice, st));
+                launch_check_finite(stage_k.p, cfg_.kv_dtype, (int64_t)n * d, d_err_.as<int>(), kErrNonFiniteKey, st);
+                launch_check_finite(stage_v.p, cfg_.kv_dtype, (int64_t)n * d, d_err_.as<int>(), kErrNonFiniteValue, st);
+                launches_ += 2;
+                segs.clear();
+                for (int l = l0; l < l1; ++l) {
+                    const int lg = l * H + g;
+                    const size_t seg = ((size_t)b * L + l) * H + g;
+                    if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH)
+                        segs.push_back({stage_k.p, d_proj_t_.as<double>() + (size_t)lg * d * cfg_.hash_bits,
+                                        d_codes_.as<uint64_t>() + seg * nmax_ * words_});
+                    if (persistent_[lg]) {
+                        const size_t p = (size_t)b * np_ + pidx_[lg];
+                        CLO_CUDA(cudaMemcpyAsync(d_pk_.as<char>() + p * nmax_ * d * esz, stage_k.p,
+                                                 (size_t)n * d * esz, cudaMemcpyDeviceToDevice, st));
+                        CLO_CUDA(cudaMemcpyAsync(d_pv_.as<char>() + p * nmax_ * d * esz, stage_v.p,
+                                                 (size_t)n * d * esz, cudaMemcpyDeviceToDevice, st));
+                    } else if (d_kmirror_.p) {
+                        const size_t o = (size_t)b * no_ + oidx_[lg];
+                        CLO_CUDA(cudaMemcpyAsync(d_kmirror_.as<char>() + o * nmax_ * d * esz, stage_k.p,
+                                                 (size_t)n * d * esz, cudaMemcpyDeviceToDevice, st));
+                    }
+                }
+                if (!segs.empty()) {
+                    CLO_CUDA(cudaMemcpyAsync(d_segs.p, segs.data(), sizeof(EncodeSeg) * segs.size(),
+                                             cudaMemcpyHostToDevice, st));
+                    launch_encode(d_segs.as<EncodeSeg>(), (int)segs.size(), n, d, cfg_.hash_bits,
+                                  cfg_.kv_dtype, d_err_.as<int>(), st);
+                    launches_ += 1;
+                }
+                // the staging buffers and segs are reused: serialise
+                CLO_CUDA(cudaStreamSynchronize(st));
+                l0 = l1;
+            }
+        }
+    launch_window_init(view(), st);
+    launches_ += 1;
+
+    // Step-0 selection with true queries (engine.cpp:188-201).
+    for (int l = 0; l < L; ++l) {
+        if (layer_has_off_[l]) {
+            enqueue_prepare(1, l, kPrepPrefill, kKindOffloaded, st);
+            enqueue_select(1, l, st);
+            enqueue_gather(1, l, 0, st);
+        }
+        if (layer_has_pers_[l]) {
+            enqueue_prepare(0, l, kPrepPrefill, kKindPersistent, st);
+            enqueue_select(0, l, st);
+        }
+    }
+    for (int i = 0; i < 2; ++i) CLO_CUDA(cudaMemsetAsync(scratch_[i].count, 0, sizeof(int) * L, st));
+    CLO_CUDA(cudaMemsetAsync(d_step_.p, 0, sizeof(int), st));
+    CLO_CUDA(cudaStreamSynchronize(st));
+    CLO_CUDA(cudaGetLastError());
+    check_device_error();
+    prefilled_ = true;
+}
+
+void Engine::capture_graph() {
+    const clo_model_shape& s = cfg_.shape;
+    const int L = s.num_layers;
+    const uint64_t before = launches_;
+    CLO_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
+    CLO_CUDA(cudaEventRecord(ev_fork_, s_main_));
+    CLO_CUDA(cudaStreamWaitEvent(s_pref_, ev_fork_, 0));
+    bool pref_used = false;
+    for (int l = 0; l < L; ++l) {
+        if (layer_has_off_[l]) {
+            // The lookup/selection/transfer of layer l uses approximate queries,
+            // available once layer l-1 starts, i.e. after attention(l-2):
+            // it overlaps the compute of layer l-1 (speculative prefetch,
+            // engine.cpp:246-251).
+            if (l >= 2) CLO_CUDA(cudaStreamWaitEvent(s_pref_, ev_attn_[l - 2], 0));
+            enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref_);
+            enqueue_select(1, l, s_pref_);
+            enqueue_gather(1, l, 1, s_pref_);
+            CLO_CUDA(cudaEventRecord(ev_pref_[l], s_pref_));
+            pref_used = true;
+        }
+        if (layer_has_pers_[l]) {
+            enqueue_prepare(0, l, kPrepDecode, kKindPersistent, s_main_);
+            enqueue_select(0, l, s_main_);
+        }
+        if (layer_has_off_[l]) CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_pref_[l], 0));
+        launch_append(view(), l, s_main_);
+        launch_attention_engine(view(), l, s_main_);
+        launches_ += 2;
+        CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));
+    }
+    if (pref_used) {
+        CLO_CUDA(cudaEventRecord(ev_join_, s_pref_));
+        CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
+    } else {
+        CLO_CUDA(cudaEventRecord(ev_join_, s_pref_));
+        CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
+    }
+    launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
+    launches_ += 1;
+    CLO_CUDA(cudaStreamEndCapture(s_main_, &graph_));
+    CLO_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+    kernels_per_step_ = (int)(launches_ - before);
+    launches_ = before;  // captured launches are counted per replay
+    size_t nn = 0;
+    CLO_CUDA(cudaGraphGetNodes(graph_, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CLO_CUDA(cudaGraphGetNodes(graph_, nodes.data(), &nn));
+    int kn = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CLO_CUDA(cudaGraphNodeGetType(nd, &t));
+        kn += t == cudaGraphNodeTypeKernel;
+    }
+    kernels_per_step_ = kn;
+}
+
+void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
+    if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
+    if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
+    if (!io.true_q || !io.approx_q || !io.new_k || !io.new_v)
+        fail(CLO_ERR_ARGUMENT, "step inputs must be non-null");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    const clo_model_shape& s = cfg_.shape;
+    const int B = cfg_.batch, L = s.num_layers, H = s.num_kv_heads, HQ = s.num_q_heads, d = s.head_dim;
+    const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    StepDesc desc{};
+    if (io.on_host) {
+        const size_t qb = sizeof(float) * B * L * HQ * d, kb = esz * B * L * H * d;
+        CLO_CUDA(cudaMemcpyAsync(d_in_tq_.p, io.true_q, qb, cudaMemcpyHostToDevice, user));
+        CLO_CUDA(cudaMemcpyAsync(d_in_aq_.p, io.approx_q, qb, cudaMemcpyHostToDevice, user));
+        CLO_CUDA(cudaMemcpyAsync(d_in_nk_.p, io.new_k, kb, cudaMemcpyHostToDevice, user));
+        CLO_CUDA(cudaMemcpyAsync(d_in_nv_.p, io.new_v, kb, cudaMemcpyHostToDevice, user));
+        desc.true_q = d_in_tq_.as<float>();
+        desc.approx_q = d_in_aq_.as<float>();
+        desc.new_k = d_in_nk_.p;
+        desc.new_v = d_in_nv_.p;
+        desc.out = d_out_.as<float>();
+    } else {
+        desc.true_q = io.true_q;
+        desc.approx_q = io.approx_q;
+        desc.new_k = io.new_k;
+        desc.new_v = io.new_v;
+        desc.out = io.out ? io.out : d_out_.as<float>();
+    }
+    set_desc(desc, user);
+    if (!graph_exec_) capture_graph();
+    CLO_CUDA(cudaGraphLaunch(graph_exec_, user));
+    launches_ += kernels_per_step_;
+    if (io.on_host && io.out)
+        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * B * L * HQ * d, cudaMemcpyDeviceToHost, user));
+    CLO_CUDA(cudaGetLastError());
+    ++steps_;
+}
+
+void Engine::synchronize() {
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    CLO_CUDA(cudaDeviceSynchronize());
+    check_device_error();
+}
+
+void Engine::check_device_error() {
+    int err = 0;
+    CLO_CUDA(cudaMemcpy(&err, d_err_.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!err) return;
+    CLO_CUDA(cudaMemset(d_err_.p, 0, sizeof(int)));
+    if (err & kErrNonFiniteQuery) fail(CLO_ERR_NUMERIC, "non-finite query entry");
+    if (err & kErrNonFiniteKey) fail(CLO_ERR_NUMERIC, "non-finite key entry");
+    if (err & kErrNonFiniteValue) fail(CLO_ERR_NUMERIC, "non-finite value entry");
+    if (err & kErrContract) fail(CLO_ERR_CONTRACT, "device-side contract violation");
+    fail(CLO_ERR_INTERNAL, "device-side error flag " + std::to_string(err));
+}
+
+uint64_t Engine::entry_bytes() const {
+    return 2ull * (uint64_t)cfg_.k * cfg_.shape.head_dim * cfg_.shape.bytes_per_element;
+}
+
+int Engine::held_tokens() const {  // SinkRecentBuffer::held_tokens (similarity_cache.cpp:113-118)
+    const int n = cfg_.n_prompt + steps_;
+    const int sink = std::min(n, cfg_.sink_tokens);
+    return sink + std::min(n - sink, cfg_.recent_tokens);
+}
+
+template <typename T>
+static std::vector<T> fetch(const DevBuf& b, size_t count, size_t offset = 0) {
+    std::vector<T> out(count);
+    if (count) CLO_CUDA(cudaMemcpy(out.data(), b.as<T>() + offset, sizeof(T) * count, cudaMemcpyDeviceToHost));
+    return out;
+}
+
+clo_metrics Engine::metrics() {
+    synchronize();
+    const clo_model_shape& s = cfg_.shape;
+    const size_t segs = (size_t)cfg_.batch * s.num_layers * s.num_kv_heads;
+    auto hits = fetch<unsigned long long>(d_hits_, segs);
+    auto misses = fetch<unsigned long long>(d_misses_, segs);
+    auto gathered = fetch<unsigned long long>(d_gathered_, 1);
+    clo_metrics m{};
+    m.steps = steps_;
+    for (size_t i = 0; i < segs; ++i) {
+        m.hits += hits[i];
+        m.misses += misses[i];
+    }
+    m.lookups = m.hits + m.misses;
+    m.hit_ratio = m.lookups ? (double)m.hits / (double)m.lookups : 0.0;
+    m.transferred_bytes = m.misses * entry_bytes();
+    m.persistent_bytes = (uint64_t)cfg_.batch * np_ * steps_ * entry_bytes();
+    m.gathered_bytes_device = gathered[0];
+    const uint64_t rows = (uint64_t)cfg_.n_prompt + steps_;
+    const uint64_t row_bytes = 2ull * s.head_dim * s.bytes_per_element;
+    m.host_bytes = (uint64_t)no_ * rows * row_bytes;
+    m.device_persistent_bytes = (uint64_t)np_ * rows * row_bytes;
+    m.cache_bytes_current =
+        steps_ == 0 ? 0
+                    : clo_cache_bytes(no_, cfg_.k, no_ ? held_tokens() : 0, s.num_layers, s.num_q_heads,
+                                      s.head_dim, s.bytes_per_element);
+    m.sync_mode = sync_mode_;
+    return m;
+}
+
+clo_head_state Engine::head_state(int b, int l, int g, int32_t* entry_indices, double* history) {
+    const clo_model_shape& s = cfg_.shape;
+    if (b < 0 || b >= cfg_.batch || l < 0 || l >= s.num_layers || g < 0 || g >= s.num_kv_heads)
+        fail(CLO_ERR_INDEX, "head out of range");
+    synchronize();
+    const size_t seg = ((size_t)b * s.num_layers + l) * s.num_kv_heads + g;
+    const int lg = l * s.num_kv_heads + g;
+    const int m = s.num_q_heads / s.num_kv_heads;
+    clo_head_state st{};
+    st.placement = persistent_[lg] ? CLO_PLACEMENT_PERSISTENT : CLO_PLACEMENT_OFFLOADED;
+    st.hits = fetch<unsigned long long>(d_hits_, 1, seg)[0];
+    st.misses = fetch<unsigned long long>(d_misses_, 1, seg)[0];
+    st.transferred_bytes = persistent_[lg] ? 0 : st.misses * entry_bytes();
+    st.persistent_bytes = persistent_[lg] ? steps_ * entry_bytes() : 0;
+    st.last_update_step = fetch<int>(d_cache_last_, 1, seg)[0];
+    st.entry_last_update_step = fetch<int>(d_entry_last_, 1, seg)[0];
+    auto valid = fetch<int>(d_label_valid_, m, ((size_t)b * s.num_layers + l) * s.num_q_heads + (size_t)g * m);
+    st.labels_valid = 0;
+    for (int v : valid) st.labels_valid += v != 0;
+    st.window_held_tokens = persistent_[lg] ? 0 : held_tokens();
+    const bool has_history = !persistent_[lg] && cfg_.policy == CLO_POLICY_SIMILARITY;
+    st.n_history = has_history ? steps_ : 0;
+    if (entry_indices) {
+        auto idx = fetch<int32_t>(d_entry_idx_, cfg_.k, seg * cfg_.k);
+        std::copy(idx.begin(), idx.end(), entry_indices);
+    }
+    if (history && st.n_history) {
+        auto h = fetch<double>(d_history_, st.n_history, seg * std::max(cfg_.max_steps, 1));
+        std::copy(h.begin(), h.end(), history);
+    }
+    return st;
+}
+
+void Engine::entry_rows(int b, int l, int g, void* k_rows, void* v_rows) {
+    const clo_model_shape& s = cfg_.shape;
+    if (b < 0 || b >= cfg_.batch || l < 0 || l >= s.num_layers || g < 0 || g >= s.num_kv_heads)
+        fail(CLO_ERR_INDEX, "head out of range");
+    const int lg = l * s.num_kv_heads + g;
+    if (persistent_[lg]) fail(CLO_ERR_ARGUMENT, "persistent heads have no cache entry");
+    synchronize();
+    const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    const size_t bytes = (size_t)cfg_.k * s.head_dim * esz;
+    const size_t o = (size_t)b * no_ + oidx_[lg];
+    if (k_rows) CLO_CUDA(cudaMemcpy(k_rows, d_slot_k_.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
+    if (v_rows) CLO_CUDA(cudaMemcpy(v_rows, d_slot_v_.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
+}
+
+static void json_num(std::ostringstream& os, double v) {
+    char buf[64];
+    if (v == std::floor(v) && std::fabs(v) < 1e15) {
+        std::snprintf(buf, sizeof buf, "%.1f", v);
+    } else {
+        std::snprintf(buf, sizeof buf, "%.17g", v);
+    }
+    os << buf;
+}
+
+std::string Engine::cache_state_json(int b) {
+    // engine.cpp:464-530, same keys and nesting.
+    const clo_model_shape& s = cfg_.shape;
+    if (b < 0 || b >= cfg_.batch) fail(CLO_ERR_INDEX, "sequence out of range");
+    clo_metrics tot{};
+    {
+        synchronize();
+        const size_t L = s.num_layers, H = s.num_kv_heads;
+        auto hits = fetch<unsigned long long>(d_hits_, L * H, (size_t)b * L * H);
+        auto misses = fetch<unsigned long long>(d_misses_, L * H, (size_t)b * L * H);
+        for (size_t i = 0; i < L * H; ++i) {
+            tot.hits += hits[i];
+            tot.misses += misses[i];
+        }
+    }
+    clo_metrics all = metrics();
+    const uint64_t lookups = tot.hits + tot.misses;
+    std::ostringstream os;
+    os << "{\n  \"policy\": \"" << (cfg_.policy == CLO_POLICY_SIMILARITY ? "similarity" : "prefetch_only")
+       << "\",\n  \"sync_mode\": \"" << (sync_mode_ == CLO_SYNC_GPU_CENTRIC ? "gpu_centric" : "cpu_centric")
+       << "\",\n  \"k\": " << cfg_.k << ",\n  \"sink_tokens\": " << cfg_.sink_tokens
+       << ",\n  \"recent_tokens\": " << cfg_.recent_tokens << ",\n  \"steps_run\": " << steps_
+       << ",\n  \"totals\": {\n    \"hits\": " << tot.hits << ",\n    \"misses\": " << tot.misses
+       << ",\n    \"hit_ratio\": ";
+    json_num(os, lookups ? (double)tot.hits / (double)lookups : 0.0);
+    os << ",\n    \"transferred_bytes\": " << tot.misses * entry_bytes()
+       << ",\n    \"persistent_served_bytes\": " << (uint64_t)np_ * steps_ * entry_bytes()
+       << ",\n    \"cache_bytes\": " << all.cache_bytes_current << ",\n    \"host_bytes\": " << all.host_bytes
+       << ",\n    \"device_persistent_bytes\": " << all.device_persistent_bytes
+       << ",\n    \"mean_output_error\": 0.0\n  },\n  \"layers\": [";
+    std::vector<int32_t> idx(cfg_.k);
+    std::vector<double> hist(std::max(cfg_.max_steps, 1));
+    for (int l = 0; l < s.num_layers; ++l) {
+        os << (l ? "," : "") << "\n    {\n      \"layer\": " << l << ",\n      \"heads\": [";
+        for (int g = 0; g < s.num_kv_heads; ++g) {
+            clo_head_state st = head_state(b, l, g, idx.data(), hist.data());
+            const bool off = st.placement == CLO_PLACEMENT_OFFLOADED;
+            os << (g ? "," : "") << "\n        {\n          \"kv_head\": " << g << ",\n          \"placement\": \""
+               << (off ? "offloaded" : "persistent") << "\",\n          \"hits\": " << st.hits
+               << ",\n          \"misses\": " << st.misses << ",\n          \"transferred_bytes\": "
+               << st.transferred_bytes << ",\n          \"persistent_served_bytes\": " << st.persistent_bytes;
+            if (off) {
+                os << ",\n          \"window_held_tokens\": " << st.window_held_tokens;
+                if (cfg_.policy == CLO_POLICY_SIMILARITY) {
+                    os << ",\n          \"entry_indices\": [";
+                    for (int i = 0; i < cfg_.k; ++i) os << (i ? ", " : "") << idx[i];
+                    os << "],\n          \"entry_last_update_step\": " << st.entry_last_update_step
+                       << ",\n          \"labels_valid\": " << st.labels_valid
+                       << ",\n          \"aggregated_history\": [";
+                    for (int i = 0; i < st.n_history; ++i) {
+                        if (i) os << ", ";
+                        json_num(os, hist[i]);
+                    }
+                    os << "]";
+                }
+            }
+            os << "\n        }";
+        }
+        os << "\n      ]\n    }";
+    }
+    os << "\n  ]\n}";
+    return os.str();
+}
+
+}  // namespace clo

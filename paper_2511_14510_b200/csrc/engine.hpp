@@ -1,0 +1,89 @@
+// engine.hpp — host-side B200 DecodeEngine (mirrors kvsim::DecodeEngine,
+// engine.hpp:91-139 of the reference).
+#pragma once
+
+#include <array>
+#include <string>
+#include <vector>
+
+#include "clo.h"
+#include "common.cuh"
+#include "engine_view.h"
+#include "host_common.hpp"
+#include "select.cuh"
+
+namespace clo {
+
+class Engine {
+  public:
+    Engine(const clo_engine_config& cfg, const double* tau, const double* q_importance,
+           const int* persistent);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride);
+    void prefill(const float* true_q0, int on_host, cudaStream_t user);
+    void decode_step(const clo_step_io& io, cudaStream_t user);
+    void synchronize();
+    clo_metrics metrics();
+    clo_head_state head_state(int b, int l, int g, int32_t* entry_indices, double* history);
+    void entry_rows(int b, int l, int g, void* k_rows, void* v_rows);
+    std::string cache_state_json(int b);
+
+    uint64_t launches() const { return launches_; }
+    int kernels_per_step() const { return kernels_per_step_; }
+    const clo_engine_config& config() const { return cfg_; }
+
+  private:
+    static constexpr int kDescRing = 256;
+
+    void allocate();
+    EngineView view() const;
+    SelArgs sel_args(int which, int layer) const;
+    void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
+    void enqueue_select(int which, int layer, cudaStream_t st);
+    void enqueue_gather(int which, int layer, int count_bytes, cudaStream_t st);
+    void capture_graph();
+    void set_desc(const StepDesc& d, cudaStream_t st);
+    void check_device_error();
+    uint64_t entry_bytes() const;
+    int held_tokens() const;
+
+    clo_engine_config cfg_;
+    std::vector<double> tau_, qimp_;
+    std::vector<int> persistent_, pidx_, oidx_, layer_has_pers_, layer_has_off_;
+    int np_ = 0, no_ = 0;
+    int sync_mode_ = CLO_SYNC_GPU_CENTRIC;
+    int nmax_ = 0, max_chunks_ = 0, words_ = 0, nb_ = 0, max_attn_chunks_ = 0;
+
+    void* host_k_ = nullptr;
+    void* host_v_ = nullptr;
+    int64_t seq_stride_ = 0, layer_stride_ = 0, head_stride_ = 0;
+
+    DevBuf d_persistent_, d_pidx_, d_oidx_, d_tau_, d_qimp_;
+    DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;
+    DevBuf d_entry_idx_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
+    DevBuf d_hits_, d_misses_, d_cache_last_, d_entry_last_, d_last_hit_, d_history_, d_gathered_;
+    DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_;
+    DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
+    std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
+    std::array<std::array<DevBuf, 12>, 2> scratch_bufs_;
+
+    cudaStream_t s_main_ = nullptr, s_pref_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    std::vector<cudaEvent_t> ev_attn_, ev_pref_;
+    cudaGraph_t graph_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    StepDesc* desc_host_ = nullptr;
+    std::vector<cudaEvent_t> desc_ev_;
+    std::vector<int> desc_used_;
+    int desc_next_ = 0;
+
+    bool prefilled_ = false;
+    int steps_ = 0;
+    uint64_t launches_ = 0;
+    int kernels_per_step_ = 0;
+};
+
+}  // namespace clo

@@ -1,0 +1,105 @@
+// engine_view.h — POD view of the engine's device state, passed by value to
+// every engine kernel. Layouts (all row-major; s = (b*L + l)*H + g is the
+// segment = one (sequence, layer, KV head) unit of the reference's per-head
+// loops, engine.cpp:260-409):
+//
+//   host_k/host_v   pinned UVA host KV of every head (HeadStore::k/v):
+//                   base + b*seq_stride + l*layer_stride + g*head_stride + row*d
+//   pk/pv           [B*NP][nmax][d]   persistent heads' full KV in HBM
+//   kmirror         [B*NO][nmax][d]   exact retriever only: HBM copy of the
+//                                     offloaded heads' K (parity mode)
+//   slot_k/slot_v   [B*NO][k][d]      cache-entry rows (CacheEntry::k_rows/v_rows)
+//   win_k/win_v     [B*NO][sink+recent][d]  SinkRecentBuffer (sink rows, then ring)
+//   entry_idx       [B*L*H][k] int32  offloaded: CacheEntry::indices;
+//                                     persistent: this step's selection
+//   codes           [B*L*H][nmax][words] u64 sign-hash bits (RetrievalMetadata::bits)
+//   proj_t          [L*H][d][bits] f64  projection transposed (P^T)
+//   labels          [B*L*hq][d] f64, label_valid [B*L*hq]   (QueryLabel)
+//   tau [L*H], qimp [L*H][m]                       (HeadProfileEntry)
+//   seg counters    hits/misses [B*L*H] u64, last_update/entry_last_update,
+//                   last_lookup_hit, history [B*L*H][max_steps] f64
+#pragma once
+
+#include <stdint.h>
+
+namespace clo {
+
+struct SelItem;
+
+struct StepDesc {
+    const float* true_q;   // [B][L][hq][d]
+    const float* approx_q; // [B][L][hq][d]
+    const void* new_k;     // [B][L][H][d]
+    const void* new_v;
+    float* out;            // [B][L][hq][d]
+};
+
+// Per-stream selection scratch (one for the prefetch stream, one for the
+// compute stream).
+struct SelScratch {
+    int* count;            // [L] items appended by prepare for layer l
+    SelItem* items;        // [B*H] work items (select.cuh)
+    double* q64;           // [B*H][m][d] widened queries of each item
+    uint64_t* qbits;       // [B*H][m][words]
+    uint16_t* key16;       // [B*H][nmax] sign-hash scores S(i)
+    uint64_t* key64;       // [B*H][nmax] exact: orderable keys of S(i)
+    uint32_t* chunk_hist;  // [B*H][max_chunks][nb]
+    int* chunk_base;       // [B*H][max_chunks]
+    int* chunk_take;       // [B*H][max_chunks]
+    uint64_t* thresh;      // [B*H] threshold key T
+    int* need;             // [B*H] ties to take / remaining k during radix passes
+    uint32_t* radix_hist;  // [B*H][256] exact radix pass histogram
+};
+
+struct EngineView {
+    // shape
+    int B, L, H, HQ, m, d, k, sink, recent, bits, words, nb;
+    int n_prompt, nmax, max_steps, max_chunks;
+    int retriever, policy, always_miss, always_hit, has_tau_override;
+    double tau_override;
+    int kv_dtype;
+    int NP, NO;            // persistent / offloaded (l,g) pairs
+    // host KV
+    const void* host_k;
+    const void* host_v;
+    void* host_k_w;        // same pointers, writable (append)
+    void* host_v_w;
+    int64_t seq_stride, layer_stride, head_stride;
+    // placement
+    const int* persistent; // [L*H]
+    const int* pidx;       // [L*H] index among persistent (l,g) or -1
+    const int* oidx;       // [L*H] index among offloaded (l,g) or -1
+    // HBM stores
+    void* pk;
+    void* pv;
+    void* kmirror;
+    void* slot_k;
+    void* slot_v;
+    void* win_k;
+    void* win_v;
+    int32_t* entry_idx;
+    uint64_t* codes;
+    const double* proj_t;
+    double* labels;
+    int* label_valid;
+    const double* tau;
+    const double* qimp;
+    // metrics
+    unsigned long long* hits;
+    unsigned long long* misses;
+    int* cache_last_update;
+    int* entry_last_update;
+    int* last_lookup_hit;
+    double* history;
+    unsigned long long* gathered_bytes;
+    // step state
+    int* dev_step;         // completed decode steps
+    const StepDesc* desc;
+    int* err;
+    // attention partials
+    float* attn_part;      // [B*H][max_attn_chunks][m][d + 2]
+    int* attn_count;       // [B*H] arrival counters (self-resetting)
+    int max_attn_chunks;
+};
+
+}  // namespace clo

@@ -1,0 +1,487 @@
+// select.cu — K1 `score_select`: key scoring and bit-exact top-k selection.
+// See select.cuh for the semantics and the reference functions restated.
+#include <cub/block/block_scan.cuh>
+
+#include "select.cuh"
+
+namespace clo {
+
+namespace {
+
+constexpr int kWarps = kScoreThreads / 32;
+constexpr int kRowsPerThread = kScoreChunk / kScoreThreads;  // 16
+
+__device__ __forceinline__ int num_chunks(int n) { return (n + kScoreChunk - 1) / kScoreChunk; }
+
+// ---------------------------------------------------------------- sign-hash
+
+// S(i) = max_j (bits - popcount(q_j ^ code_i)) (hamming_affinity,
+// retrieval.cpp:27-31) for every key of one 4096-row chunk, written as u16,
+// plus the chunk's histogram of S (per-warp smem histograms, then summed).
+template <int W>
+__global__ void __launch_bounds__(kScoreThreads) score_signhash_kernel(SelArgs a) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* whist = smem;                                   // [kWarps][nb]
+    uint64_t* qb = reinterpret_cast<uint64_t*>(smem + kWarps * a.nb + (kWarps * a.nb & 1));
+    const int units = *a.count * a.max_chunks;
+    const int warp = threadIdx.x >> 5;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) continue;
+        const int end = min(start + kScoreChunk, it.n);
+        for (int i = threadIdx.x; i < kWarps * a.nb; i += blockDim.x) whist[i] = 0;
+        for (int i = threadIdx.x; i < a.m * W; i += blockDim.x) {
+            const int j = i / W, w = i % W;
+            qb[i] = a.qbits[((size_t)item * a.m + j) * a.words + w];
+        }
+        __syncthreads();
+        const uint64_t* codes = it.codes;
+        uint16_t* keys = a.key16 + (size_t)item * a.nmax;
+        uint32_t* myhist = whist + warp * a.nb;
+#pragma unroll 4
+        for (int r = start + threadIdx.x; r < end; r += kScoreThreads) {
+            uint64_t c[W];
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(codes + (size_t)r * W);
+            if constexpr (W % 2 == 0) {
+#pragma unroll
+                for (int w = 0; w < W / 2; ++w) {
+                    ulonglong2 v = __ldg(src + w);
+                    c[2 * w] = v.x;
+                    c[2 * w + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < W; ++w) c[w] = __ldg(codes + (size_t)r * W + w);
+            }
+            int best = 0;
+            for (int j = 0; j < a.m; ++j) {
+                int dist = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qb[j * W + w]);
+                best = max(best, a.bits - dist);
+            }
+            keys[r] = static_cast<uint16_t>(best);
+            atomicAdd(&myhist[best], 1u);
+        }
+        __syncthreads();
+        uint32_t* out = a.chunk_hist + ((size_t)item * a.max_chunks + chunk) * a.nb;
+        for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s += whist[w * a.nb + b];
+            out[b] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// Per item: T = k-th largest S (ties resolved later by index), then each
+// chunk's output offset and how many of its S == T ties it keeps.
+__global__ void __launch_bounds__(1024) threshold_signhash_kernel(SelArgs a) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* tot = smem;                               // [nb]
+    int* gt = reinterpret_cast<int*>(smem + a.nb);      // [max_chunks]
+    int* eq = gt + a.max_chunks;                        // [max_chunks]
+    __shared__ int sT, sGt;
+    const int count = *a.count;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+        const SelItem it = a.items[item];
+        const int nch = num_chunks(it.n);
+        const uint32_t* hist = a.chunk_hist + (size_t)item * a.max_chunks * a.nb;
+        for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
+            uint32_t s = 0;
+            for (int c = 0; c < nch; ++c) s += hist[(size_t)c * a.nb + b];
+            tot[b] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // Walk bins from the top in blocks of 32: suffix sums by warp scan.
+            int running = 0, T = -1, gtT = 0;
+            for (int top = a.nb - 1; top >= 0 && T < 0; top -= 32) {
+                const int b = top - lane;
+                int v = b >= 0 ? (int)tot[b] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= a.k);
+                if (hit) {
+                    const int first = __ffs(hit) - 1;
+                    const int excl = __shfl_sync(0xffffffffu, incl - v, first);
+                    T = top - first;
+                    gtT = running + excl;
+                }
+                running += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) {
+                sT = T;
+                sGt = gtT;
+            }
+        }
+        __syncthreads();
+        const int T = sT, need_eq = a.k - sGt;
+        for (int c = warp; c < nch; c += nwarps) {
+            const uint32_t* h = hist + (size_t)c * a.nb;
+            int g = 0;
+            for (int b = T + 1 + lane; b < a.nb; b += 32) g += h[b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+            if (lane == 0) {
+                gt[c] = g;
+                eq[c] = h[T];
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int base_run = 0, eq_run = 0;
+            for (int c0 = 0; c0 < nch; c0 += 32) {
+                const int c = c0 + lane;
+                const int e = c < nch ? eq[c] : 0;
+                int ie = e;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, ie, o);
+                    if (lane >= o) ie += t;
+                }
+                const int eq_before = eq_run + ie - e;
+                const int take = max(0, min(e, need_eq - eq_before));
+                const int contrib = c < nch ? gt[c] + take : 0;
+                int ic = contrib;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, ic, o);
+                    if (lane >= o) ic += t;
+                }
+                if (c < nch) {
+                    a.chunk_base[(size_t)item * a.max_chunks + c] = base_run + ic - contrib;
+                    a.chunk_take[(size_t)item * a.max_chunks + c] = take;
+                }
+                base_run += __shfl_sync(0xffffffffu, ic, 31);
+                eq_run += __shfl_sync(0xffffffffu, ie, 31);
+            }
+            if (lane == 0) {
+                a.thresh[item] = (uint64_t)T;
+                a.need[item] = need_eq;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- compaction
+
+template <typename KeyT>
+__device__ __forceinline__ double key_score(KeyT k);
+template <>
+__device__ __forceinline__ double key_score<uint16_t>(uint16_t k) { return (double)k; }
+template <>
+__device__ __forceinline__ double key_score<uint64_t>(uint64_t k) { return key_to_double(k); }
+
+// Keeps S > T and the first chunk_take ties S == T (index order) of one chunk,
+// writing indices ascending at chunk_base (select_topk's final ascending sort,
+// retrieval.cpp:43, merge_group_topk's :197-199).
+template <typename KeyT>
+__global__ void __launch_bounds__(kScoreThreads) compact_kernel(SelArgs a) {
+    using Scan = cub::BlockScan<int, kScoreThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) continue;
+        const KeyT T = (KeyT)a.thresh[item];
+        const int take = a.chunk_take[(size_t)item * a.max_chunks + chunk];
+        const int base = a.chunk_base[(size_t)item * a.max_chunks + chunk];
+        const KeyT* keys = (sizeof(KeyT) == 2 ? (const KeyT*)(a.key16 + (size_t)item * a.nmax)
+                                              : (const KeyT*)(a.key64 + (size_t)item * a.nmax));
+        const int r0 = start + threadIdx.x * kRowsPerThread;
+        KeyT kv[kRowsPerThread];
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) {
+            const int r = r0 + i;
+            kv[i] = r < it.n ? keys[r] : (KeyT)0;
+        }
+        int n_eq = 0;
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) n_eq += (r0 + i < it.n && kv[i] == T);
+        int eq_prefix;
+        Scan(scan_tmp).ExclusiveSum(n_eq, eq_prefix);
+        __syncthreads();
+        unsigned selmask = 0;
+        int e = eq_prefix;
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) {
+            if (r0 + i >= it.n) continue;
+            bool s = kv[i] > T;
+            if (kv[i] == T) {
+                s = e < take;
+                ++e;
+            }
+            if (s) selmask |= 1u << i;
+        }
+        int pos;
+        Scan(scan_tmp).ExclusiveSum(__popc(selmask), pos);
+        __syncthreads();
+        pos += base;
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) {
+            if (selmask & (1u << i)) {
+                it.out_idx[pos] = r0 + i;
+                if (it.out_score) it.out_score[pos] = key_score<KeyT>(kv[i]);
+                ++pos;
+            }
+        }
+    }
+}
+
+// -------------------------------------------------------------------- exact
+
+// S(i) = max_j sum_c q_j[c]*K[i][c] (retrieval.cpp:101-106, sequential IEEE
+// double without FMA) -> orderable u64 key. Chunk 0 of each item also resets
+// the radix state.
+template <typename T>
+__global__ void __launch_bounds__(kScoreThreads) score_exact_kernel(SelArgs a) {
+    extern __shared__ double qs[];  // [m][d]
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) continue;
+        const int end = min(start + kScoreChunk, it.n);
+        if (chunk == 0) {
+            for (int b = threadIdx.x; b < 256; b += blockDim.x) a.radix_hist[(size_t)item * 256 + b] = 0;
+            if (threadIdx.x == 0) {
+                a.need[item] = a.k;
+                a.thresh[item] = 0;
+            }
+        }
+        for (int i = threadIdx.x; i < a.m * a.d; i += blockDim.x)
+            qs[i] = a.q64[(size_t)item * a.m * a.d + i];
+        __syncthreads();
+        const T* rows = static_cast<const T*>(it.rows);
+        uint64_t* keys = a.key64 + (size_t)item * a.nmax;
+        for (int r = start + threadIdx.x; r < end; r += blockDim.x) {
+            const T* kr = rows + (size_t)r * a.d;
+            double best = 0.0;
+            for (int j = 0; j < a.m; ++j) {
+                double s = 0.0;
+                for (int c = 0; c < a.d; ++c) s = dmac(s, qs[j * a.d + c], to_f64<T>(kr[c]));
+                if (j == 0 || s > best) best = s;
+            }
+            keys[r] = orderable_key(best);
+        }
+        __syncthreads();
+    }
+}
+
+// One MSB-first 8-bit radix pass: histogram digit `shift` of the keys whose
+// higher digits equal the prefix found so far.
+__global__ void __launch_bounds__(kScoreThreads) radix_hist_kernel(SelArgs a, int shift) {
+    __shared__ uint32_t h[256];
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) continue;
+        const int end = min(start + kScoreChunk, it.n);
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+        __syncthreads();
+        const uint64_t prefix = a.thresh[item];
+        const uint64_t* keys = a.key64 + (size_t)item * a.nmax;
+        for (int r = start + threadIdx.x; r < end; r += blockDim.x) {
+            const uint64_t key = keys[r];
+            if (shift == 56 || ((key ^ prefix) >> (shift + 8)) == 0)
+                atomicAdd(&h[(key >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 256; b += blockDim.x)
+            if (h[b]) atomicAdd(&a.radix_hist[(size_t)item * 256 + b], h[b]);
+        __syncthreads();
+    }
+}
+
+// Picks the digit holding the need-th largest key, narrows the prefix and
+// resets the histogram for the next pass.
+__global__ void radix_pick_kernel(SelArgs a, int shift) {
+    const int count = *a.count;
+    const int lane = threadIdx.x;
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+        uint32_t* h = a.radix_hist + (size_t)item * 256;
+        const int need = a.need[item];
+        int running = 0, D = -1, above = 0;
+        for (int top = 255; top >= 0 && D < 0; top -= 32) {
+            const int b = top - lane;
+            const int v = (int)h[b];
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, running + incl >= need);
+            if (hit) {
+                const int first = __ffs(hit) - 1;
+                above = running + __shfl_sync(0xffffffffu, incl - v, first);
+                D = top - first;
+            }
+            running += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        for (int b = lane; b < 256; b += 32) h[b] = 0;
+        if (lane == 0) {
+            a.need[item] = need - above;
+            a.thresh[item] |= (uint64_t)D << shift;
+        }
+    }
+}
+
+// Per chunk: count keys > T and == T (exact path; T complete after 8 passes).
+__global__ void __launch_bounds__(kScoreThreads) count_chunks_kernel(SelArgs a) {
+    using Scan = cub::BlockScan<int, kScoreThreads>;
+    __shared__ int sg[kWarps], se[kWarps];
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) continue;
+        const int end = min(start + kScoreChunk, it.n);
+        const uint64_t T = a.thresh[item];
+        const uint64_t* keys = a.key64 + (size_t)item * a.nmax;
+        int g = 0, e = 0;
+        for (int r = start + threadIdx.x; r < end; r += blockDim.x) {
+            const uint64_t key = keys[r];
+            g += key > T;
+            e += key == T;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+            e += __shfl_xor_sync(0xffffffffu, e, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            sg[threadIdx.x >> 5] = g;
+            se[threadIdx.x >> 5] = e;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int G = 0, E = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                G += sg[w];
+                E += se[w];
+            }
+            uint32_t* out = a.chunk_hist + ((size_t)item * a.max_chunks + chunk) * 2;
+            out[0] = G;
+            out[1] = E;
+        }
+        __syncthreads();
+    }
+}
+
+// Per item: chunk offsets and tie quotas from the (gt, eq) counts.
+__global__ void chunk_prefix_kernel(SelArgs a) {
+    const int count = *a.count;
+    const int lane = threadIdx.x;
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+        const SelItem it = a.items[item];
+        const int nch = num_chunks(it.n);
+        const int need_eq = a.need[item];
+        int base_run = 0, eq_run = 0;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+            const int c = c0 + lane;
+            const uint32_t* h = a.chunk_hist + ((size_t)item * a.max_chunks + c) * 2;
+            const int g = c < nch ? (int)h[0] : 0;
+            const int e = c < nch ? (int)h[1] : 0;
+            int ie = e;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, ie, o);
+                if (lane >= o) ie += t;
+            }
+            const int take = max(0, min(e, need_eq - (eq_run + ie - e)));
+            const int contrib = g + take;
+            int ic = contrib;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, ic, o);
+                if (lane >= o) ic += t;
+            }
+            if (c < nch) {
+                a.chunk_base[(size_t)item * a.max_chunks + c] = base_run + ic - contrib;
+                a.chunk_take[(size_t)item * a.max_chunks + c] = take;
+            }
+            base_run += __shfl_sync(0xffffffffu, ic, 31);
+            eq_run += __shfl_sync(0xffffffffu, ie, 31);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
+    const size_t sm_score = (size_t)kWarps * a.nb * 4 + 8 + (size_t)a.m * a.words * 8;
+    switch (a.words) {
+#define CLO_W(W)                                                                        \
+    case W:                                                                             \
+        score_signhash_kernel<W><<<a.grid, kScoreThreads, sm_score, stream>>>(a);       \
+        break;
+        CLO_W(1) CLO_W(2) CLO_W(3) CLO_W(4) CLO_W(5) CLO_W(6) CLO_W(7) CLO_W(8)
+#undef CLO_W
+        default:
+            break;
+    }
+    const size_t sm_thr = (size_t)a.nb * 4 + (size_t)a.max_chunks * 8;
+    int items_grid = a.grid < 1024 ? a.grid : 1024;
+    threshold_signhash_kernel<<<items_grid, 1024, sm_thr, stream>>>(a);
+    compact_kernel<uint16_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
+}
+
+void launch_select_exact(const SelArgs& a, cudaStream_t stream) {
+    const size_t sm_q = (size_t)a.m * a.d * 8;
+    switch (a.dtype) {
+        case kBF16:
+            score_exact_kernel<__nv_bfloat16><<<a.grid, kScoreThreads, sm_q, stream>>>(a);
+            break;
+        case kF32:
+            score_exact_kernel<float><<<a.grid, kScoreThreads, sm_q, stream>>>(a);
+            break;
+        default:
+            score_exact_kernel<double><<<a.grid, kScoreThreads, sm_q, stream>>>(a);
+            break;
+    }
+    int items_grid = a.grid < 1024 ? a.grid : 1024;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        radix_hist_kernel<<<a.grid, kScoreThreads, 0, stream>>>(a, shift);
+        radix_pick_kernel<<<items_grid, 32, 0, stream>>>(a, shift);
+    }
+    count_chunks_kernel<<<a.grid, kScoreThreads, 0, stream>>>(a);
+    chunk_prefix_kernel<<<items_grid, 32, 0, stream>>>(a);
+    compact_kernel<uint64_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
+}
+
+namespace {
+__global__ void __launch_bounds__(256) hash_queries_kernel(const double* q64, int m, int d,
+                                                           const double* proj_t, int bits,
+                                                           int words, uint64_t* qbits) {
+    extern __shared__ double qs[];
+    for (int i = threadIdx.x; i < m * d; i += blockDim.x) qs[i] = q64[i];
+    __syncthreads();
+    hash_queries_block(qs, m, d, proj_t, bits, words, qbits);
+}
+}  // namespace
+
+void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, int bits,
+                         int words, uint64_t* qbits, cudaStream_t stream) {
+    hash_queries_kernel<<<1, 256, (size_t)m * d * sizeof(double), stream>>>(q64, m, d, proj_t,
+                                                                            bits, words, qbits);
+}
+
+}  // namespace clo

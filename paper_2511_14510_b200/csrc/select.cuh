@@ -1,0 +1,89 @@
+// select.cuh — key scoring + top-k selection (K1 `score_select`).
+//
+// Semantics: DecodeEngine::group_topk (engine.cpp:211-223) = m calls of
+// retrieve_scored (retrieval.cpp:90-125, select_topk :33-46) followed by
+// merge_group_topk (similarity_cache.cpp:180-201). That equals ONE top-k over
+// S(i) = max_j score_j(i) under (S desc, i asc), reported ascending
+// (DESIGN.md §3 has the proof). The GPU computes it as:
+//   score      S(i) per key -> u16 (sign-hash, S in [0, bits]) or orderable
+//              u64 (exact, S a double), plus per-chunk histograms
+//   threshold  sign-hash: T = the k-th largest S from the histograms;
+//              exact: 8 MSB-first radix passes over the u64 keys
+//   compact    keep S > T, plus the first `need` ties S == T in index order,
+//              written ascending at per-chunk offsets (a two-level scan)
+// Every result is an integer function of the bit-exact scores, so indices
+// match the reference bit for bit.
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace clo {
+
+struct SelItem {
+    int seg;                // engine segment (or 0 for op-level calls)
+    int n;                  // pool size: rows [0, n) are candidates
+    const void* rows;       // exact: K rows [n][d] of dtype
+    const uint64_t* codes;  // sign-hash: bits [n][words]
+    int32_t* out_idx;       // [k] ascending selection
+    double* out_score;      // [k] S(out_idx) or nullptr
+};
+
+struct SelArgs {
+    const SelItem* items;
+    const int* count;       // number of valid items
+    int m, d, k, bits, words, nb, nmax, max_chunks, dtype;
+    const double* q64;      // [item][m][d]
+    const uint64_t* qbits;  // [item][m][words]
+    uint16_t* key16;        // [item][nmax]
+    uint64_t* key64;        // [item][nmax]
+    uint32_t* chunk_hist;   // [item][max_chunks][nb]   (exact: [..][2] gt/eq)
+    int* chunk_base;        // [item][max_chunks]
+    int* chunk_take;        // [item][max_chunks]
+    uint64_t* thresh;       // [item]
+    int* need;              // [item]
+    uint32_t* radix_hist;   // [item][256]
+    int grid;               // CTAs for the grid-stride kernels
+};
+
+// Host launchers (select.cu). All enqueue on `stream`; no host sync.
+void launch_select_signhash(const SelArgs& a, cudaStream_t stream);
+void launch_select_exact(const SelArgs& a, cudaStream_t stream);
+// Query sign bits for op-level calls (one CTA): q64 [m][d] -> qbits [m][words].
+void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, int bits,
+                         int words, uint64_t* qbits, cudaStream_t stream);
+
+// Sign bits of m queries (append_sign_row semantics, retrieval.cpp:14-25,
+// as used for the query bits at :113-119): bit b = (sum_c P[b][c]*q[c]) >= 0
+// summed sequentially in IEEE double. Called by a whole CTA (blockDim.x a
+// multiple of 32). q64 [m][d] (smem), proj_t [d][bits] -> qbits [m][words].
+__device__ __forceinline__ void hash_queries_block(const double* q64, int m, int d,
+                                                   const double* proj_t, int bits, int words,
+                                                   uint64_t* qbits_out) {
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(qbits_out);
+    const int total = words * 64;
+    for (int b0 = 0; b0 < total; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        double s[kMaxGroup];
+#pragma unroll
+        for (int j = 0; j < kMaxGroup; ++j) s[j] = 0.0;
+        if (b < bits) {
+            for (int c = 0; c < d; ++c) {
+                const double p = proj_t[(size_t)c * bits + b];
+#pragma unroll
+                for (int j = 0; j < kMaxGroup; ++j)
+                    if (j < m) s[j] = dmac(s[j], p, q64[j * d + c]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxGroup; ++j) {
+            if (j < m) {
+                const unsigned bal = __ballot_sync(0xffffffffu, b < bits && s[j] >= 0.0);
+                if ((threadIdx.x & 31) == 0 && b < total) out32[j * words * 2 + (b >> 5)] = bal;
+            }
+        }
+    }
+}
+
+}  // namespace clo

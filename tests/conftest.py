@@ -1,0 +1,35 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: longer-running case")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle.bind import Oracle, build
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        build(ref=False)
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def reference():
+    from oracle.bind import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libkvsim_ref.so not built (needs /root/reference at build time)")
+    return Reference()
+
+
+@pytest.fixture(scope="session")
+def clo():
+    from paper_2511_14510_b200 import _lib
+    return _lib.load()

@@ -1,0 +1,123 @@
+"""Engine-level parity: the CUDA DecodeEngine vs the CPU oracle (clo_oracle.c,
+itself pinned to the reference) on identical inputs, stepped in lockstep.
+Bit-exact: entry indices, hit/miss decisions, aggregated similarity history,
+label state, gathered rows. Outputs: relative L2 <= 1e-3 (f32 storage) /
+2e-2 (bf16 storage), the north-star tolerances."""
+import json
+
+import numpy as np
+import pytest
+
+from tests.engine_harness import gpu_engine, make_case, run_and_compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kv_dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("retriever", ["sign_hash", "exact"])
+def test_similarity_policy_matches_oracle(oracle, kv_dtype, retriever):
+    case = make_case(kv_dtype=kv_dtype, retriever=retriever)
+    g, o, worst = run_and_compare(case, oracle)
+    m = g.metrics()
+    assert 0 < m["hits"] and 0 < m["misses"], m  # both decisions exercised
+    assert worst < 1e-5  # fp32 accumulation over identical widened inputs
+
+
+def test_forced_miss_exact_matches_standalone_oracle(oracle):
+    # acceptance criterion 4 (acceptance_main.cpp:142-206): always_miss, exact
+    # retriever, no cross-layer drift -> outputs equal the standalone top-k oracle.
+    case = make_case(L=4, hq=4, hkv=2, d=32, n_prompt=160, steps=20, k=13, retriever="exact",
+                     always_miss=True, kv_dtype="f32", sink=4, recent=64)
+    g, o, worst = run_and_compare(case, oracle)
+    m = g.metrics()
+    offloaded_heads = 3 * 2
+    assert m["hits"] == 0 and m["misses"] == offloaded_heads * 20 * case["cfg"].batch
+    entry_bytes = 2 * 13 * 32 * 4
+    assert m["transferred_bytes"] == m["misses"] * entry_bytes
+    assert m["gathered_bytes_device"] == m["transferred_bytes"]  # byte conservation (crit. 11)
+    assert m["persistent_bytes"] == case["cfg"].batch * 2 * 20 * entry_bytes
+    assert worst <= 1e-5
+
+
+def test_threshold_floor_hits_everywhere(oracle):
+    # engine_test.cpp:46-59: tau = -1 -> every lookup hits, nothing transferred.
+    # small drift keeps every cosine positive (a non-positive one still misses,
+    # similarity_cache.cpp:57-60)
+    case = make_case(tau=-1.0, steps=12, sigma_step=0.05)
+    g, o, _ = run_and_compare(case, oracle)
+    m = g.metrics()
+    assert m["hit_ratio"] == 1.0 and m["misses"] == 0 and m["transferred_bytes"] == 0
+    assert m["hits"] == 2 * 2 * 12 * case["cfg"].batch
+    assert m["sync_mode"] == 1  # GPU-centric for the similarity policy
+
+
+def test_forced_hits_freeze_step0_entry(oracle):
+    # engine_test.cpp:88-104
+    case = make_case(always_hit=True)
+    g, o, _ = run_and_compare(case, oracle)
+    for l in range(1, 3):
+        for gg in range(2):
+            st = g.head(l, gg)
+            assert st["entry_last_update_step"] == 0 and st["last_update_step"] == 0
+
+
+def test_prefetch_only_policy(oracle):
+    # engine_test.cpp:106-118
+    case = make_case(policy="prefetch_only")
+    g, o, _ = run_and_compare(case, oracle)
+    m = g.metrics()
+    assert m["hits"] == 0 and m["misses"] == 2 * 2 * 12 * case["cfg"].batch
+    assert m["sync_mode"] == 0  # CPU-centric default for non-similarity policies
+
+
+def test_persistent_plan_and_window_clamp(oracle):
+    # heads persisted in several layers; window wider than part of the prompt
+    pers = np.array([[1, 1], [0, 1], [1, 0]], np.int32)
+    case = make_case(persistent=pers, sink=4, recent=64, n_prompt=72, k=16, steps=10)
+    run_and_compare(case, oracle)
+
+
+def test_gqa_groups_of_five_and_d128(oracle):
+    # Qwen-style m = 5 (40q/8kv scaled down), d = 128, bf16
+    case = make_case(L=2, hq=10, hkv=2, d=128, n_prompt=300, steps=6, k=32, kv_dtype="bf16",
+                     sink=4, recent=64, batch=2)
+    run_and_compare(case, oracle)
+
+
+def test_cache_state_json_matches_oracle_layout(oracle):
+    case = make_case(steps=8)
+    g, o, _ = run_and_compare(case, oracle)
+    doc = json.loads(g.cache_state_json(0))
+    assert doc["policy"] == "similarity" and doc["sync_mode"] == "gpu_centric"
+    assert doc["steps_run"] == 8
+    assert len(doc["layers"]) == 3
+    assert doc["layers"][0]["heads"][0]["placement"] == "persistent"
+    h = doc["layers"][1]["heads"][0]
+    assert h["placement"] == "offloaded"
+    assert len(h["entry_indices"]) == 8 and len(h["aggregated_history"]) == 8
+    ost = o[0][0].head_state(1, 0)
+    assert h["entry_indices"] == list(map(int, ost["entry_indices"]))
+    assert h["aggregated_history"] == list(map(float, ost["aggregated_history"]))
+
+
+def test_decode_past_end_and_before_prefill_raise():
+    from paper_2511_14510_b200._lib import ContractError
+    case = make_case(steps=2)
+    g = gpu_engine(case)
+    with pytest.raises(ContractError):
+        g.decode_step()
+    g.prefill()
+    g.decode_step()
+    g.decode_step()
+    with pytest.raises(ContractError):
+        g.decode_step()
+
+
+def test_non_finite_step_input_raises_numeric_error():
+    from paper_2511_14510_b200._lib import NumericError
+    case = make_case(steps=3)
+    case["wl"].true_q[1, 0, 1, 0, 0] = np.nan
+    g = gpu_engine(case)
+    g.prefill()
+    with pytest.raises(NumericError):
+        g.decode_step()
