@@ -211,6 +211,18 @@ clo_status clo_get_entry_rows(clo_engine* e, int seq, int layer, int kv_head, vo
  * Writes at most cap bytes (NUL-terminated); *needed gets the full size. */
 clo_status clo_cache_state_json(clo_engine* e, int seq, char* buf, size_t cap, size_t* needed);
 
+/* One decode step (same semantics as clo_decode_step) through an instrumented
+ * copy of the step graph with event-record nodes around every kernel; fills
+ * one record per kernel launch with its device time. Synchronous. Used by the
+ * benchmark to measure per-kernel rooflines inside the graph. */
+typedef struct clo_kernel_time {
+    char name[32];
+    int layer;
+    float ms;
+} clo_kernel_time;
+clo_status clo_engine_profile_step(clo_engine* e, const clo_step_io* io, void* stream,
+                                   clo_kernel_time* out, int cap, int* count);
+
 /* Number of sm_100a kernels the engine enqueued since creation. */
 uint64_t clo_engine_kernel_launches(const clo_engine* e);
 /* Kernels per decode step (graph nodes that are kernels). */

@@ -354,7 +354,7 @@ class Reference(_Common):
         return outs[: cfg.steps], buf.value.decode(), secs[: cfg.steps]
 
     def bench_units(self, cfg: EngineCfg, tau, q_importance, prompt_k, prompt_v, true_q,
-                    approx_q, new_k, new_v, threads):
+                    approx_q, new_k, new_v, threads, warmup=0):
         arrs = [np.ascontiguousarray(a, np.float64) for a in
                 (q_importance, prompt_k, prompt_v, true_q, approx_q, new_k, new_v)]
         qi, pk, pv, tq, aq, nk, nv = arrs
@@ -363,5 +363,6 @@ class Reference(_Common):
         self._check(self.lib.ref_bench_units(
             C.byref(cfg), C.c_double(tau), _p(qi, C.c_double), _p(pk, C.c_double),
             _p(pv, C.c_double), _p(tq, C.c_double), _p(aq, C.c_double), _p(nk, C.c_double),
-            _p(nv, C.c_double), C.c_int(threads), _p(sps, C.c_double), _p(pre, C.c_double)))
+            _p(nv, C.c_double), C.c_int(threads), C.c_int(warmup), _p(sps, C.c_double),
+            _p(pre, C.c_double)))
         return sps, pre

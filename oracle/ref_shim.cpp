@@ -348,12 +348,13 @@ int ref_run_engine(const ref_engine_cfg* c, const double* tau, const double* q_i
 // m query heads, offloaded, similarity policy), run concurrently the way the
 // reference runner runs independent engines on a std::thread pool
 // (runner.cpp:186-278). Inputs are caller arrays shared by all threads.
-// Returns per-thread mean seconds per decode_step in sec_per_step[threads]
-// and the prefill seconds in prefill_seconds[threads].
+// The first `warmup` decode steps are untimed. Returns per-thread mean seconds
+// per timed decode_step in sec_per_step[threads] and the prefill seconds in
+// prefill_seconds[threads].
 int ref_bench_units(const ref_engine_cfg* c, double tau, const double* q_importance,
                     const double* prompt_k, const double* prompt_v, const double* true_q,
                     const double* approx_q, const double* new_k, const double* new_v,
-                    int threads, double* sec_per_step, double* prefill_seconds) {
+                    int threads, int warmup, double* sec_per_step, double* prefill_seconds) {
     std::vector<int> status(threads, 0);
     std::vector<std::string> errs(threads);
     std::vector<std::thread> pool;
@@ -374,10 +375,11 @@ int ref_bench_units(const ref_engine_cfg* c, double tau, const double* q_importa
                 engine.prefill();
                 auto p1 = std::chrono::steady_clock::now();
                 prefill_seconds[w] = std::chrono::duration<double>(p1 - p0).count();
+                for (int t = 0; t < warmup; ++t) engine.decode_step();
                 auto t0 = std::chrono::steady_clock::now();
-                for (int t = 0; t < c->steps; ++t) engine.decode_step();
+                for (int t = warmup; t < c->steps; ++t) engine.decode_step();
                 auto t1 = std::chrono::steady_clock::now();
-                sec_per_step[w] = std::chrono::duration<double>(t1 - t0).count() / c->steps;
+                sec_per_step[w] = std::chrono::duration<double>(t1 - t0).count() / (c->steps - warmup);
             });
             if (status[w]) errs[w] = g_err;
         });

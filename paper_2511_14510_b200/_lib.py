@@ -111,6 +111,10 @@ class HeadState(C.Structure):
     ]
 
 
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("layer", C.c_int), ("ms", C.c_float)]
+
+
 _P = C.c_void_p
 _I = C.c_int
 _I64 = C.c_int64
@@ -130,6 +134,7 @@ SIGNATURES = {
     "clo_get_head_state": (_I, [_P, _I, _I, _I, C.POINTER(HeadState), _P, _P]),
     "clo_get_entry_rows": (_I, [_P, _I, _I, _I, _P, _P]),
     "clo_cache_state_json": (_I, [_P, _I, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "clo_engine_profile_step": (_I, [_P, C.POINTER(StepIO), _P, C.POINTER(KernelTime), _I, C.POINTER(_I)]),
     "clo_engine_kernel_launches": (_U64, [_P]),
     "clo_engine_kernels_per_step": (_I, [_P]),
     "clo_engine_attach_nccl": (_I, [_P, _P, _I, _I]),

@@ -179,6 +179,17 @@ clo_status clo_cache_state_json(clo_engine* e, int seq, char* buf, size_t cap, s
     });
 }
 
+clo_status clo_engine_profile_step(clo_engine* e, const clo_step_io* io, void* stream,
+                                   clo_kernel_time* out, int cap, int* count) {
+    return guarded([&] {
+        if (!io) fail(CLO_ERR_ARGUMENT, "null step io");
+        auto recs = ENG->profile_step(*io, static_cast<cudaStream_t>(stream));
+        const int n = (int)std::min<size_t>(recs.size(), cap > 0 ? (size_t)cap : 0);
+        for (int i = 0; i < n; ++i) out[i] = recs[i];
+        if (count) *count = (int)recs.size();
+    });
+}
+
 uint64_t clo_engine_kernel_launches(const clo_engine* e) {
     return reinterpret_cast<const Engine*>(e)->launches();
 }

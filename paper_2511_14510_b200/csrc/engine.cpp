@@ -104,6 +104,12 @@ Engine::~Engine() {
     cudaSetDevice(cfg_.device);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (graph_) cudaGraphDestroy(graph_);
+    if (pgraph_exec_) cudaGraphExecDestroy(pgraph_exec_);
+    if (pgraph_) cudaGraphDestroy(pgraph_);
+    for (auto& r : prof_) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
     for (auto ev : ev_attn_) cudaEventDestroy(ev);
     for (auto ev : ev_pref_) cudaEventDestroy(ev);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -338,8 +344,28 @@ SelArgs Engine::sel_args(int which, int layer) const {
     return a;
 }
 
+void Engine::prof_begin(cudaStream_t st) {
+    if (!profiling_capture_) return;
+    if (prof_used_ == prof_.size()) {
+        ProfRec r{};
+        CLO_CUDA(cudaEventCreate(&r.a));
+        CLO_CUDA(cudaEventCreate(&r.b));
+        prof_.push_back(r);
+    }
+    CLO_CUDA(cudaEventRecordWithFlags(prof_[prof_used_].a, st, cudaEventRecordExternal));
+}
+
+void Engine::prof_end(cudaStream_t st, const char* name, int layer) {
+    if (!profiling_capture_) return;
+    ProfRec& r = prof_[prof_used_++];
+    r.name = name;
+    r.layer = layer;
+    CLO_CUDA(cudaEventRecordWithFlags(r.b, st, cudaEventRecordExternal));
+}
+
 void Engine::enqueue_select(int which, int layer, cudaStream_t st) {
     SelArgs a = sel_args(which, layer);
+    prof_begin(st);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
         launch_select_signhash(a, st);
         launches_ += 3;
@@ -347,6 +373,7 @@ void Engine::enqueue_select(int which, int layer, cudaStream_t st) {
         launch_select_exact(a, st);
         launches_ += 21;
     }
+    prof_end(st, which ? "select_offloaded" : "select_persistent", layer);
 }
 
 void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st) {
@@ -356,7 +383,9 @@ void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStrea
     pa.layer = layer;
     pa.mode = mode;
     pa.kind = kind;
+    prof_begin(st);
     launch_prepare(pa, st);
+    prof_end(st, which ? "lookup_offloaded" : "lookup_persistent", layer);
     launches_ += 1;
 }
 
@@ -370,7 +399,9 @@ void Engine::enqueue_gather(int which, int layer, int count_bytes, cudaStream_t 
     const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
     const int64_t vecs = (int64_t)cfg_.k * cfg_.shape.head_dim * esz / 16;
     const int64_t units = (int64_t)cfg_.batch * cfg_.shape.num_kv_heads * ((vecs + 1023) / 1024);
+    prof_begin(st);
     launch_gather_engine(ga, grid_for(units), st);
+    prof_end(st, "gather_zero_copy", layer);
     launches_ += 1;
 }
 
@@ -395,6 +426,12 @@ void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_st
         cudaGraphDestroy(graph_);
         graph_exec_ = nullptr;
         graph_ = nullptr;
+    }
+    if (pgraph_exec_) {
+        cudaGraphExecDestroy(pgraph_exec_);
+        cudaGraphDestroy(pgraph_);
+        pgraph_exec_ = nullptr;
+        pgraph_ = nullptr;
     }
 }
 
@@ -506,10 +543,12 @@ void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
     prefilled_ = true;
 }
 
-void Engine::capture_graph() {
+void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_t* exec_out) {
     const clo_model_shape& s = cfg_.shape;
     const int L = s.num_layers;
     const uint64_t before = launches_;
+    profiling_capture_ = profiled;
+    prof_used_ = 0;
     CLO_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
     CLO_CUDA(cudaEventRecord(ev_fork_, s_main_));
     CLO_CUDA(cudaStreamWaitEvent(s_pref_, ev_fork_, 0));
@@ -532,8 +571,12 @@ void Engine::capture_graph() {
             enqueue_select(0, l, s_main_);
         }
         if (layer_has_off_[l]) CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_pref_[l], 0));
+        prof_begin(s_main_);
         launch_append(view(), l, s_main_);
+        prof_end(s_main_, "append", l);
+        prof_begin(s_main_);
         launch_attention_engine(view(), l, s_main_);
+        prof_end(s_main_, "attention", l);
         launches_ += 2;
         CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));
     }
@@ -546,14 +589,14 @@ void Engine::capture_graph() {
     }
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
-    CLO_CUDA(cudaStreamEndCapture(s_main_, &graph_));
-    CLO_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
-    kernels_per_step_ = (int)(launches_ - before);
+    CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
+    profiling_capture_ = false;
+    CLO_CUDA(cudaGraphInstantiate(exec_out, *graph_out, 0));
     launches_ = before;  // captured launches are counted per replay
     size_t nn = 0;
-    CLO_CUDA(cudaGraphGetNodes(graph_, nullptr, &nn));
+    CLO_CUDA(cudaGraphGetNodes(*graph_out, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
-    CLO_CUDA(cudaGraphGetNodes(graph_, nodes.data(), &nn));
+    CLO_CUDA(cudaGraphGetNodes(*graph_out, nodes.data(), &nn));
     int kn = 0;
     for (auto nd : nodes) {
         cudaGraphNodeType t;
@@ -563,12 +606,7 @@ void Engine::capture_graph() {
     kernels_per_step_ = kn;
 }
 
-void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
-    if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
-    if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
-    if (!io.true_q || !io.approx_q || !io.new_k || !io.new_v)
-        fail(CLO_ERR_ARGUMENT, "step inputs must be non-null");
-    CLO_CUDA(cudaSetDevice(cfg_.device));
+StepDesc Engine::make_desc(const clo_step_io& io, cudaStream_t user) {
     const clo_model_shape& s = cfg_.shape;
     const int B = cfg_.batch, L = s.num_layers, H = s.num_kv_heads, HQ = s.num_q_heads, d = s.head_dim;
     const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
@@ -591,8 +629,45 @@ void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
         desc.new_v = io.new_v;
         desc.out = io.out ? io.out : d_out_.as<float>();
     }
-    set_desc(desc, user);
-    if (!graph_exec_) capture_graph();
+    return desc;
+}
+
+std::vector<clo_kernel_time> Engine::profile_step(const clo_step_io& io, cudaStream_t user) {
+    if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
+    if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    const clo_model_shape& s = cfg_.shape;
+    set_desc(make_desc(io, user), user);
+    if (!pgraph_exec_) capture_graph(true, &pgraph_, &pgraph_exec_);
+    CLO_CUDA(cudaGraphLaunch(pgraph_exec_, user));
+    launches_ += kernels_per_step_;
+    if (io.on_host && io.out)
+        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * cfg_.batch * s.num_layers * s.num_q_heads * s.head_dim,
+                                 cudaMemcpyDeviceToHost, user));
+    ++steps_;
+    CLO_CUDA(cudaStreamSynchronize(user));
+    check_device_error();
+    std::vector<clo_kernel_time> out;
+    for (size_t i = 0; i < prof_used_; ++i) {
+        clo_kernel_time kt{};
+        std::snprintf(kt.name, sizeof kt.name, "%s", prof_[i].name);
+        kt.layer = prof_[i].layer;
+        CLO_CUDA(cudaEventElapsedTime(&kt.ms, prof_[i].a, prof_[i].b));
+        out.push_back(kt);
+    }
+    return out;
+}
+
+void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
+    if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
+    if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
+    if (!io.true_q || !io.approx_q || !io.new_k || !io.new_v)
+        fail(CLO_ERR_ARGUMENT, "step inputs must be non-null");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    const clo_model_shape& s = cfg_.shape;
+    const int B = cfg_.batch, L = s.num_layers, HQ = s.num_q_heads, d = s.head_dim;
+    set_desc(make_desc(io, user), user);
+    if (!graph_exec_) capture_graph(false, &graph_, &graph_exec_);
     CLO_CUDA(cudaGraphLaunch(graph_exec_, user));
     launches_ += kernels_per_step_;
     if (io.on_host && io.out)

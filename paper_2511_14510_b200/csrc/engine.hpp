@@ -31,6 +31,11 @@ class Engine {
     void entry_rows(int b, int l, int g, void* k_rows, void* v_rows);
     std::string cache_state_json(int b);
 
+    // One decode step through an instrumented copy of the step graph: external
+    // event-record nodes around every kernel, so per-launch device time is
+    // measured inside the graph (bench roofline). Synchronous.
+    std::vector<clo_kernel_time> profile_step(const clo_step_io& io, cudaStream_t user);
+
     uint64_t launches() const { return launches_; }
     int kernels_per_step() const { return kernels_per_step_; }
     const clo_engine_config& config() const { return cfg_; }
@@ -44,7 +49,10 @@ class Engine {
     void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
     void enqueue_select(int which, int layer, cudaStream_t st);
     void enqueue_gather(int which, int layer, int count_bytes, cudaStream_t st);
-    void capture_graph();
+    void capture_graph(bool profiled, cudaGraph_t* graph, cudaGraphExec_t* exec);
+    void prof_begin(cudaStream_t st);
+    void prof_end(cudaStream_t st, const char* name, int layer);
+    StepDesc make_desc(const clo_step_io& io, cudaStream_t user);
     void set_desc(const StepDesc& d, cudaStream_t st);
     void check_device_error();
     uint64_t entry_bytes() const;
@@ -75,6 +83,17 @@ class Engine {
     std::vector<cudaEvent_t> ev_attn_, ev_pref_;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
+    cudaGraph_t pgraph_ = nullptr;
+    cudaGraphExec_t pgraph_exec_ = nullptr;
+    bool profiling_capture_ = false;
+    struct ProfRec {
+        cudaEvent_t a, b;
+        const char* name;
+        int layer;
+    };
+    std::vector<ProfRec> prof_;
+    std::vector<cudaEvent_t> prof_pending_;
+    size_t prof_used_ = 0;
     StepDesc* desc_host_ = nullptr;
     std::vector<cudaEvent_t> desc_ev_;
     std::vector<int> desc_used_;

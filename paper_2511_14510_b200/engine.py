@@ -200,8 +200,9 @@ class DecodeEngine:
         nmax = self.n_prompt + self.steps
         Lk = 1 if getattr(source, "alias_layers", False) else L
         self.hkv = host_kv or HostKV(cfg.batch, Lk, H, nmax, s.head_dim, cfg.kv_dtype)
-        self.hkv.k[:, :, :, : self.n_prompt] = source.prompt_k
-        self.hkv.v[:, :, :, : self.n_prompt] = source.prompt_v
+        if source.prompt_k is not None:  # None: the caller filled host_kv itself
+            self.hkv.k[:, :, :, : self.n_prompt] = source.prompt_k
+            self.hkv.v[:, :, :, : self.n_prompt] = source.prompt_v
         ss, ls, hs = self.hkv.strides
         check(self.lib.clo_engine_bind_host_kv(self.h, self.hkv.k.ctypes.data, self.hkv.v.ctypes.data,
                                                ss, 0 if Lk == 1 else ls, hs))
