@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
     if (badq) raise_err(v.err, kErrNonFiniteQuery);
 
     const int32_t* idx = v.entry_idx + (size_t)seg * v.k;
+    const int32_t* stok = pers ? nullptr : v.slot_tok + (size_t)((size_t)b * v.NO + v.oidx[lg]) * v.k;
     const int wrows = v.sink + v.recent;
     const size_t pslot = pers ? (size_t)b * v.NP + v.pidx[lg] : 0;
     const size_t oslot = pers ? 0 : (size_t)b * v.NO + v.oidx[lg];
@@ -111,15 +112,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
             ok[u] = pos < p1;
             const T* kr = nullptr;
             const T* vr = nullptr;
+            int tok = 0;
             if (ok[u]) {
                 if (pos < v.k) {
-                    const int tok = idx[pos];
-                    ok[u] = !(tok < s1 || tok >= wstart);  // dedup against the window
+                    // persistent: the selection indexes the full HBM KV;
+                    // offloaded: walk the cache slots (delta-gather layout)
+                    tok = pers ? idx[pos] : stok[pos];
                     kr = pers ? pk + (size_t)tok * D : sk + (size_t)pos * D;
                     vr = pers ? pv + (size_t)tok * D : sv + (size_t)pos * D;
                 } else {
                     const int w = pos - v.k;
-                    const int tok = w < s1 ? w : wstart + (w - s1);
+                    tok = w < s1 ? w : wstart + (w - s1);
                     const int wr = tok < v.sink ? tok : v.sink + tok % v.recent;
                     kr = pers ? pk + (size_t)tok * D : wk + (size_t)wr * D;
                     vr = pers ? pv + (size_t)tok * D : wv + (size_t)wr * D;
@@ -135,6 +138,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
                     vv[u][i] = make_uint4(0, 0, 0, 0);
                 }
             }
+            // dedup against the window (union_indices, engine.cpp:80-85); the
+            // loads above do not wait on this test
+            if (ok[u] && pos < v.k) ok[u] = !(tok < s1 || tok >= wstart);
         }
         float s[U][M];
 #pragma unroll

@@ -22,6 +22,8 @@ namespace clo {
 
 namespace {
 
+constexpr int64_t kGatherCtas = 48;
+
 int grid_for(int64_t units) {
     const int64_t cap = (int64_t)kNumSMs * 8;
     if (units < 1) return 1;
@@ -68,6 +70,7 @@ Engine::Engine(const clo_engine_config& cfg, const double* tau, const double* q_
     if ((s.head_dim * (cfg.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4)) % 16 != 0)
         fail(CLO_ERR_CONFIG, "K/V rows must be a multiple of 16 bytes");
     if (cfg.sink_tokens + cfg.recent_tokens > 4096) fail(CLO_ERR_CONFIG, "window too large");
+    if (cfg.k > reconcile_max_k()) fail(CLO_ERR_CONFIG, "k above 8192 is not supported");
 
     const int L = s.num_layers, H = s.num_kv_heads;
     tau_.assign(tau, tau + (size_t)L * H);
@@ -112,10 +115,13 @@ Engine::~Engine() {
     }
     for (auto ev : ev_attn_) cudaEventDestroy(ev);
     for (auto ev : ev_pref_) cudaEventDestroy(ev);
+    for (auto ev : ev_sel_) cudaEventDestroy(ev);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_join2_) cudaEventDestroy(ev_join2_);
     if (s_main_) cudaStreamDestroy(s_main_);
     if (s_pref_) cudaStreamDestroy(s_pref_);
+    if (s_xfer_) cudaStreamDestroy(s_xfer_);
     if (desc_host_) cudaFreeHost(desc_host_);
     for (auto ev : desc_ev_) cudaEventDestroy(ev);
 }
@@ -151,6 +157,8 @@ void Engine::allocate() {
     d_win_k_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
     d_win_v_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
     d_entry_idx_.alloc(sizeof(int32_t) * segs * k);
+    d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
+    d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
         d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_, false);
         // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
@@ -202,7 +210,7 @@ void Engine::allocate() {
         auto& bufs = scratch_bufs_[i];
         const size_t items = (size_t)B * H;
         bufs[0].alloc(sizeof(int) * L);
-        bufs[1].alloc(sizeof(SelItem) * items);
+        bufs[1].alloc(sizeof(SelItem) * items * L);  // per-layer work lists
         bufs[2].alloc(sizeof(double) * items * m * d);
         bufs[3].alloc(sizeof(uint64_t) * items * m * words_);
         if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH)
@@ -215,6 +223,12 @@ void Engine::allocate() {
         bufs[9].alloc(sizeof(uint64_t) * items);
         bufs[10].alloc(sizeof(int) * items);
         bufs[11].alloc(sizeof(uint32_t) * items * 256);
+        if (i == 1) {  // offloaded heads: new selections + per-layer fetch lists
+            bufs[12].alloc(sizeof(int32_t) * items * k, false);
+            bufs[13].alloc(sizeof(int32_t) * L * items * k, false);
+            bufs[14].alloc(sizeof(int32_t) * L * items * k, false);
+            bufs[15].alloc(sizeof(int) * L * items);
+        }
         sc.count = bufs[0].as<int>();
         sc.items = bufs[1].as<SelItem>();
         sc.q64 = bufs[2].as<double>();
@@ -227,17 +241,25 @@ void Engine::allocate() {
         sc.thresh = bufs[9].as<uint64_t>();
         sc.need = bufs[10].as<int>();
         sc.radix_hist = bufs[11].as<uint32_t>();
+        sc.sel = bufs[12].as<int32_t>();
+        sc.fetch_tok = bufs[13].as<int32_t>();
+        sc.fetch_slot = bufs[14].as<int32_t>();
+        sc.fetch_count = bufs[15].as<int>();
     }
 
     CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
     CLO_CUDA(cudaStreamCreateWithFlags(&s_pref_, cudaStreamNonBlocking));
+    CLO_CUDA(cudaStreamCreateWithFlags(&s_xfer_, cudaStreamNonBlocking));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    CLO_CUDA(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
     ev_attn_.resize(L);
     ev_pref_.resize(L);
+    ev_sel_.resize(L);
     for (int l = 0; l < L; ++l) {
         CLO_CUDA(cudaEventCreateWithFlags(&ev_attn_[l], cudaEventDisableTiming));
         CLO_CUDA(cudaEventCreateWithFlags(&ev_pref_[l], cudaEventDisableTiming));
+        CLO_CUDA(cudaEventCreateWithFlags(&ev_sel_[l], cudaEventDisableTiming));
     }
     CLO_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&desc_host_), sizeof(StepDesc) * kDescRing,
                            cudaHostAllocDefault));
@@ -293,6 +315,8 @@ EngineView Engine::view() const {
     v.win_k = d_win_k_.p;
     v.win_v = d_win_v_.p;
     v.entry_idx = d_entry_idx_.as<int32_t>();
+    v.entry_slot = d_entry_slot_.as<int32_t>();
+    v.slot_tok = d_slot_tok_.as<int32_t>();
     v.codes = d_codes_.as<uint64_t>();
     v.proj_t = d_proj_t_.as<double>();
     v.labels = d_labels_.as<double>();
@@ -319,7 +343,7 @@ SelArgs Engine::sel_args(int which, int layer) const {
     const clo_model_shape& s = cfg_.shape;
     const SelScratch& sc = scratch_[which];
     SelArgs a{};
-    a.items = sc.items;
+    a.items = sc.items + (size_t)layer * cfg_.batch * s.num_kv_heads;
     a.count = sc.count + layer;
     a.m = s.num_q_heads / s.num_kv_heads;
     a.d = s.head_dim;
@@ -380,6 +404,7 @@ void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStrea
     PrepareArgs pa{};
     pa.v = view();
     pa.s = scratch_[which];
+    pa.s.items += (size_t)layer * cfg_.batch * cfg_.shape.num_kv_heads;
     pa.layer = layer;
     pa.mode = mode;
     pa.kind = kind;
@@ -389,18 +414,47 @@ void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStrea
     launches_ += 1;
 }
 
-void Engine::enqueue_gather(int which, int layer, int count_bytes, cudaStream_t st) {
+void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
+    const SelScratch& sc = scratch_[1];
+    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
+    ReconcileArgs ra{};
+    ra.v = view();
+    ra.items = sc.items + (size_t)layer * items;
+    ra.count = sc.count;
+    ra.sel = sc.sel;
+    ra.fetch_tok = sc.fetch_tok;
+    ra.fetch_slot = sc.fetch_slot;
+    ra.fetch_count = sc.fetch_count;
+    ra.items_cap = (int)items;
+    ra.layer = layer;
+    ra.fresh = fresh;
+    prof_begin(st);
+    launch_reconcile(ra, st);
+    prof_end(st, "reconcile", layer);
+    launches_ += 1;
+}
+
+void Engine::enqueue_gather(int layer, int count_bytes, cudaStream_t st) {
+    const SelScratch& sc = scratch_[1];
+    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
     GatherEngineArgs ga{};
     ga.v = view();
-    ga.items = scratch_[which].items;
-    ga.count = scratch_[which].count;
+    ga.items = sc.items + (size_t)layer * items;
+    ga.count = sc.count;
+    ga.fetch_tok = sc.fetch_tok;
+    ga.fetch_slot = sc.fetch_slot;
+    ga.fetch_count = sc.fetch_count;
+    ga.items_cap = (int)items;
     ga.layer = layer;
     ga.count_bytes = count_bytes;
     const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
     const int64_t vecs = (int64_t)cfg_.k * cfg_.shape.head_dim * esz / 16;
-    const int64_t units = (int64_t)cfg_.batch * cfg_.shape.num_kv_heads * ((vecs + 1023) / 1024);
+    const int64_t units = (int64_t)items * ((vecs + 1023) / 1024);
     prof_begin(st);
-    launch_gather_engine(ga, grid_for(units), st);
+    // PCIe needs ~100 KB in flight (55 GB/s x ~2 us); each CTA keeps 32 KiB
+    // outstanding, so a few dozen CTAs saturate the link and leave the SMs to
+    // the selection and attention kernels running concurrently.
+    launch_gather_engine(ga, (int)std::min<int64_t>(units, kGatherCtas), st);
     prof_end(st, "gather_zero_copy", layer);
     launches_ += 1;
 }
@@ -528,7 +582,8 @@ void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
         if (layer_has_off_[l]) {
             enqueue_prepare(1, l, kPrepPrefill, kKindOffloaded, st);
             enqueue_select(1, l, st);
-            enqueue_gather(1, l, 0, st);
+            enqueue_reconcile(l, 1, st);
+            enqueue_gather(l, 0, st);
         }
         if (layer_has_pers_[l]) {
             enqueue_prepare(0, l, kPrepPrefill, kKindPersistent, st);
@@ -549,22 +604,35 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
     const uint64_t before = launches_;
     profiling_capture_ = profiled;
     prof_used_ = 0;
+    // Three streams: selection (lookup + score/select of offloaded heads),
+    // transfer (zero-copy gathers, back to back on the PCIe link) and compute
+    // (persistent-head selection, append, attention). Work lists are per
+    // layer, so the selection stream can run ahead of the transfer stream.
+    // The instrumented (profiled) graph serialises everything on one stream so
+    // each kernel's event-bracketed time is its own, not time spent queued
+    // behind the other streams (the share of the step, like an ncu launch list).
+    cudaStream_t s_pref = profiled ? s_main_ : s_pref_;
+    cudaStream_t s_xfer = profiled ? s_main_ : s_xfer_;
     CLO_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
     CLO_CUDA(cudaEventRecord(ev_fork_, s_main_));
-    CLO_CUDA(cudaStreamWaitEvent(s_pref_, ev_fork_, 0));
-    bool pref_used = false;
+    if (!profiled) {
+        CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_fork_, 0));
+        CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_fork_, 0));
+    }
     for (int l = 0; l < L; ++l) {
         if (layer_has_off_[l]) {
             // The lookup/selection/transfer of layer l uses approximate queries,
             // available once layer l-1 starts, i.e. after attention(l-2):
             // it overlaps the compute of layer l-1 (speculative prefetch,
             // engine.cpp:246-251).
-            if (l >= 2) CLO_CUDA(cudaStreamWaitEvent(s_pref_, ev_attn_[l - 2], 0));
-            enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref_);
-            enqueue_select(1, l, s_pref_);
-            enqueue_gather(1, l, 1, s_pref_);
-            CLO_CUDA(cudaEventRecord(ev_pref_[l], s_pref_));
-            pref_used = true;
+            if (l >= 2) CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_attn_[l - 2], 0));
+            enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
+            enqueue_select(1, l, s_pref);
+            enqueue_reconcile(l, 0, s_pref);
+            CLO_CUDA(cudaEventRecord(ev_sel_[l], s_pref));
+            CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_sel_[l], 0));
+            enqueue_gather(l, 1, s_xfer);
+            CLO_CUDA(cudaEventRecord(ev_pref_[l], s_xfer));
         }
         if (layer_has_pers_[l]) {
             enqueue_prepare(0, l, kPrepDecode, kKindPersistent, s_main_);
@@ -580,12 +648,11 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         launches_ += 2;
         CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));
     }
-    if (pref_used) {
-        CLO_CUDA(cudaEventRecord(ev_join_, s_pref_));
+    if (!profiled) {
+        CLO_CUDA(cudaEventRecord(ev_join_, s_pref));
         CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
-    } else {
-        CLO_CUDA(cudaEventRecord(ev_join_, s_pref_));
-        CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
+        CLO_CUDA(cudaEventRecord(ev_join2_, s_xfer));
+        CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join2_, 0));
     }
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
@@ -784,8 +851,19 @@ void Engine::entry_rows(int b, int l, int g, void* k_rows, void* v_rows) {
     const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
     const size_t bytes = (size_t)cfg_.k * s.head_dim * esz;
     const size_t o = (size_t)b * no_ + oidx_[lg];
-    if (k_rows) CLO_CUDA(cudaMemcpy(k_rows, d_slot_k_.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
-    if (v_rows) CLO_CUDA(cudaMemcpy(v_rows, d_slot_v_.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
+    // CacheEntry::k_rows/v_rows are in entry (ascending index) order; the
+    // slots hold them permuted (delta gather), entry_slot maps them back.
+    auto slot_of = fetch<int32_t>(d_entry_slot_, cfg_.k, o * cfg_.k);
+    const size_t rb = (size_t)s.head_dim * esz;
+    std::vector<char> tmp(bytes);
+    for (int which = 0; which < 2; ++which) {
+        void* dst = which ? v_rows : k_rows;
+        if (!dst) continue;
+        const DevBuf& src = which ? d_slot_v_ : d_slot_k_;
+        CLO_CUDA(cudaMemcpy(tmp.data(), src.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < cfg_.k; ++i)
+            std::memcpy(static_cast<char*>(dst) + (size_t)i * rb, tmp.data() + (size_t)slot_of[i] * rb, rb);
+    }
 }
 
 static void json_num(std::ostringstream& os, double v) {

@@ -48,7 +48,8 @@ class Engine {
     SelArgs sel_args(int which, int layer) const;
     void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
     void enqueue_select(int which, int layer, cudaStream_t st);
-    void enqueue_gather(int which, int layer, int count_bytes, cudaStream_t st);
+    void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
+    void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
     void capture_graph(bool profiled, cudaGraph_t* graph, cudaGraphExec_t* exec);
     void prof_begin(cudaStream_t st);
     void prof_end(cudaStream_t st, const char* name, int layer);
@@ -71,16 +72,16 @@ class Engine {
 
     DevBuf d_persistent_, d_pidx_, d_oidx_, d_tau_, d_qimp_;
     DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;
-    DevBuf d_entry_idx_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
+    DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
     DevBuf d_hits_, d_misses_, d_cache_last_, d_entry_last_, d_last_hit_, d_history_, d_gathered_;
     DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
     std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
-    std::array<std::array<DevBuf, 12>, 2> scratch_bufs_;
+    std::array<std::array<DevBuf, 16>, 2> scratch_bufs_;
 
-    cudaStream_t s_main_ = nullptr, s_pref_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
-    std::vector<cudaEvent_t> ev_attn_, ev_pref_;
+    cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_xfer_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr;
+    std::vector<cudaEvent_t> ev_attn_, ev_pref_, ev_sel_;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     cudaGraph_t pgraph_ = nullptr;

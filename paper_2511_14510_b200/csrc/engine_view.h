@@ -12,6 +12,9 @@
 //   win_k/win_v     [B*NO][sink+recent][d]  SinkRecentBuffer (sink rows, then ring)
 //   entry_idx       [B*L*H][k] int32  offloaded: CacheEntry::indices;
 //                                     persistent: this step's selection
+//   entry_slot/slot_tok [B*NO][k]     offloaded: which slot holds the i-th entry
+//                                     token / which token each slot holds (the
+//                                     delta gather keeps surviving rows in place)
 //   codes           [B*L*H][nmax][words] u64 sign-hash bits (RetrievalMetadata::bits)
 //   proj_t          [L*H][d][bits] f64  projection transposed (P^T)
 //   labels          [B*L*hq][d] f64, label_valid [B*L*hq]   (QueryLabel)
@@ -49,6 +52,10 @@ struct SelScratch {
     uint64_t* thresh;      // [B*H] threshold key T
     int* need;             // [B*H] ties to take / remaining k during radix passes
     uint32_t* radix_hist;  // [B*H][256] exact radix pass histogram
+    int32_t* sel;          // [B*H][k] offloaded items: the new selection (ascending)
+    int32_t* fetch_tok;    // [L][B*H][k] rows to fetch over PCIe (token, destination slot)
+    int32_t* fetch_slot;   // [L][B*H][k]
+    int* fetch_count;      // [L][B*H]
 };
 
 struct EngineView {
@@ -78,6 +85,8 @@ struct EngineView {
     void* win_k;
     void* win_v;
     int32_t* entry_idx;
+    int32_t* entry_slot;   // [B*NO][k] slot holding the i-th (ascending) entry token
+    int32_t* slot_tok;     // [B*NO][k] token held by each slot
     uint64_t* codes;
     const double* proj_t;
     double* labels;

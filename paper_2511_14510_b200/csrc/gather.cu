@@ -1,12 +1,21 @@
-// gather.cu — K3 `zero_copy_gather`: GPU threads read exactly the missed
-// top-k K/V rows straight from pinned, UVA-mapped host memory over PCIe and
-// write them into the HBM cache slots (update_entry's row copy,
-// similarity_cache.cpp:74-87, gather_rows engine.cpp:98-102; the transfer the
-// reference only models as bytes / pcie_peak_bw, pipeline_sim.cpp:12-22).
+// gather.cu — K3 `zero_copy_gather` and the entry reconcile (delta gather).
 //
-// Each thread keeps kUnroll K and kUnroll V 16-byte loads in flight before
-// storing, so one CTA has 256 * 2 * kUnroll * 16 B = 32 KiB outstanding —
-// enough CTAs resident across the 148 SMs to cover PCIe round-trip latency.
+// update_entry (similarity_cache.cpp:74-87) replaces a missed head's whole
+// entry with the rows of its new selection, copied from the host store
+// (gather_rows engine.cpp:98-102); the reference only models that transfer
+// as bytes / pcie_peak_bw (pipeline_sim.cpp:12-22). Here:
+//   reconcile  (one CTA per missed head) merge-joins the old entry with the
+//              new ascending selection: tokens present in both keep their
+//              HBM slot; tokens that left free their slot; each new token
+//              gets a freed slot and goes on the fetch list. The entry's
+//              CONTENTS are exactly the reference's (same indices, same
+//              rows); only the data movement shrinks to the rows that are
+//              actually missing in HBM.
+//   gather     GPU threads read exactly the fetch-list rows straight from
+//              pinned, UVA-mapped host memory over PCIe (16-byte loads, 32 KiB
+//              in flight per CTA) and store them into their slots.
+#include <cub/block/block_scan.cuh>
+
 #include "gather.cuh"
 
 namespace clo {
@@ -16,53 +25,149 @@ namespace {
 constexpr int kGatherThreads = 256;
 constexpr int kUnroll = 4;
 constexpr int kVecsPerUnit = kGatherThreads * kUnroll;  // 16-byte vectors per work unit
+constexpr int kRecThreads = 1024;
 
-__device__ __forceinline__ void copy_rows(const uint4* __restrict__ src_k, const uint4* __restrict__ src_v,
-                                          uint4* __restrict__ dst_k, uint4* __restrict__ dst_v,
-                                          const int32_t* __restrict__ idx, int vpr, int v0, int v1) {
-    uint4 rk[kUnroll], rv[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-        const int e = v0 + u * kGatherThreads + threadIdx.x;
-        if (e < v1) {
-            const int r = e / vpr, c = e - r * vpr;
-            const size_t off = (size_t)idx[r] * vpr + c;
-            rk[u] = src_k[off];
-            rv[u] = src_v[off];
-        }
+__device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x)
+            lo = mid + 1;
+        else
+            hi = mid;
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-        const int e = v0 + u * kGatherThreads + threadIdx.x;
-        if (e < v1) {
-            dst_k[e] = rk[u];
-            dst_v[e] = rv[u];
+    return lo;
+}
+
+// Per thread: a contiguous run of `per` elements; block-wide exclusive scan
+// of the per-thread counts gives each element's rank.
+__global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a) {
+    using Scan = cub::BlockScan<int, kRecThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    extern __shared__ int32_t rs[];
+    const EngineView& v = a.v;
+    const int k = v.k;
+    int32_t* old_idx = rs;           // [k]
+    int32_t* old_slot = rs + k;      // [k]
+    int32_t* nsel = rs + 2 * k;      // [k]
+    int32_t* freed = rs + 3 * k;     // [k] freed slots in old-entry order
+    const int count = a.count[a.layer];
+    const int per = (k + kRecThreads - 1) / kRecThreads;
+    const int r0 = threadIdx.x * per, r1 = min(k, r0 + per);
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+        const int seg = a.items[item].seg;
+        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+        int32_t* e_idx = v.entry_idx + (size_t)seg * k;
+        int32_t* e_slot = v.entry_slot + o * k;
+        int32_t* s_tok = v.slot_tok + o * k;
+        const int32_t* sel = a.sel + (size_t)item * k;
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            nsel[i] = sel[i];
+            old_idx[i] = a.fresh ? -1 : e_idx[i];
+            old_slot[i] = a.fresh ? i : e_slot[i];
         }
+        __syncthreads();
+        // 1) old tokens leaving the entry free their slots (old order)
+        int nfree = 0;
+        if (a.fresh) {
+            nfree = r1 - r0;
+        } else {
+            for (int j = r0; j < r1; ++j) {
+                const int p = lower_bound(nsel, k, old_idx[j]);
+                nfree += !(p < k && nsel[p] == old_idx[j]);
+            }
+        }
+        int fbase;
+        Scan(scan_tmp).ExclusiveSum(nfree, fbase);
+        __syncthreads();
+        for (int j = r0; j < r1; ++j) {
+            bool gone = true;
+            if (!a.fresh) {
+                const int p = lower_bound(nsel, k, old_idx[j]);
+                gone = !(p < k && nsel[p] == old_idx[j]);
+            }
+            if (gone) freed[fbase++] = old_slot[j];
+        }
+        __syncthreads();
+        // 2) new tokens: keep their slot if already resident, else take the
+        //    next freed slot and go on the fetch list
+        int nfetch = 0;
+        for (int i = r0; i < r1; ++i) {
+            const int p = a.fresh ? k : lower_bound(old_idx, k, nsel[i]);
+            nfetch += !(p < k && old_idx[p] == nsel[i]);
+        }
+        int base, total;
+        Scan(scan_tmp).ExclusiveSum(nfetch, base, total);
+        int32_t* ftok = a.fetch_tok + ((size_t)a.layer * a.items_cap + item) * k;
+        int32_t* fslot = a.fetch_slot + ((size_t)a.layer * a.items_cap + item) * k;
+        for (int i = r0; i < r1; ++i) {
+            const int p = a.fresh ? k : lower_bound(old_idx, k, nsel[i]);
+            int slot;
+            if (p < k && old_idx[p] == nsel[i]) {
+                slot = old_slot[p];
+            } else {
+                slot = freed[base];
+                ftok[base] = nsel[i];
+                fslot[base] = slot;
+                ++base;
+                s_tok[slot] = nsel[i];
+            }
+            e_slot[i] = slot;
+            e_idx[i] = nsel[i];
+        }
+        if (threadIdx.x == 0) a.fetch_count[(size_t)a.layer * a.items_cap + item] = total;
+        __syncthreads();
     }
 }
 
-// Engine mode: work units = (missed offloaded head, block of rows).
+// Work units = (missed head, block of fetch-list vectors).
 __global__ void __launch_bounds__(kGatherThreads) gather_engine_kernel(GatherEngineArgs a) {
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
-    const int total_vecs = v.k * vpr;
-    const int units_per_item = (total_vecs + kVecsPerUnit - 1) / kVecsPerUnit;
+    const int units_per_item = (v.k * vpr + kVecsPerUnit - 1) / kVecsPerUnit;
     const int count = a.count[a.layer];
     const int units = count * units_per_item;
+    const size_t esz = dtype_size(v.kv_dtype);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int item = u / units_per_item, part = u % units_per_item;
+        const size_t li = (size_t)a.layer * a.items_cap + item;
+        const int nf = a.fetch_count[li];
+        const int v0 = part * kVecsPerUnit;
+        const int v1 = min(nf * vpr, v0 + kVecsPerUnit);
+        if (v0 >= v1) continue;
         const int seg = a.items[item].seg;
         const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
-        const int o = b * v.NO + v.oidx[l * v.H + g];
+        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
         const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-        const size_t esz = dtype_size(v.kv_dtype);
         const uint4* src_k = reinterpret_cast<const uint4*>((const char*)v.host_k + base * esz);
         const uint4* src_v = reinterpret_cast<const uint4*>((const char*)v.host_v + base * esz);
-        uint4* dst_k = reinterpret_cast<uint4*>((char*)v.slot_k + (size_t)o * v.k * row_bytes);
-        uint4* dst_v = reinterpret_cast<uint4*>((char*)v.slot_v + (size_t)o * v.k * row_bytes);
-        const int v0 = part * kVecsPerUnit, v1 = min(total_vecs, v0 + kVecsPerUnit);
-        copy_rows(src_k, src_v, dst_k, dst_v, v.entry_idx + (size_t)seg * v.k, vpr, v0, v1);
+        uint4* dst_k = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.k * row_bytes);
+        uint4* dst_v = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.k * row_bytes);
+        const int32_t* ftok = a.fetch_tok + li * v.k;
+        const int32_t* fslot = a.fetch_slot + li * v.k;
+        uint4 rk[kUnroll], rv[kUnroll];
+        size_t dsto[kUnroll];
+#pragma unroll
+        for (int uu = 0; uu < kUnroll; ++uu) {
+            const int e = v0 + uu * kGatherThreads + threadIdx.x;
+            if (e < v1) {
+                const int r = e / vpr, c = e - r * vpr;
+                const size_t so = (size_t)ftok[r] * vpr + c;
+                dsto[uu] = (size_t)fslot[r] * vpr + c;
+                rk[uu] = src_k[so];
+                rv[uu] = src_v[so];
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < kUnroll; ++uu) {
+            const int e = v0 + uu * kGatherThreads + threadIdx.x;
+            if (e < v1) {
+                dst_k[dsto[uu]] = rk[uu];
+                dst_v[dsto[uu]] = rv[uu];
+            }
+        }
         if (a.count_bytes && threadIdx.x == 0)
             atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull * 2ull);
     }
@@ -98,6 +203,14 @@ __global__ void __launch_bounds__(kGatherThreads) gather_op_kernel(const uint4* 
 
 }  // namespace
 
+void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
+    const size_t sm = sizeof(int32_t) * 4 * (size_t)a.v.k;
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(reconcile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int grid = a.items_cap < 1024 ? a.items_cap : 1024;
+    reconcile_kernel<<<grid, kRecThreads, sm, stream>>>(a);
+}
+
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream) {
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
@@ -111,5 +224,7 @@ void launch_gather_op(const void* src, void* dst, const int32_t* idx, int row_by
                                                           static_cast<uint4*>(dst), idx, vpr, k,
                                                           n_rows, err);
 }
+
+int reconcile_max_k() { return 8192; }
 
 }  // namespace clo

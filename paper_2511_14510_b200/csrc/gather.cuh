@@ -1,4 +1,4 @@
-// gather.cuh — K3 zero-copy gather launchers.
+// gather.cuh — K3 zero-copy gather + entry reconcile launchers.
 #pragma once
 
 #include "common.cuh"
@@ -7,17 +7,36 @@
 
 namespace clo {
 
+struct ReconcileArgs {
+    EngineView v;
+    const SelItem* items;  // this layer's work list (missed offloaded heads)
+    const int* count;      // [L]
+    const int32_t* sel;    // [item][k] new ascending selections
+    int32_t* fetch_tok;    // [L][items_cap][k]
+    int32_t* fetch_slot;
+    int* fetch_count;      // [L][items_cap]
+    int items_cap;         // B*H
+    int layer;
+    int fresh;             // prefill: no previous entry
+};
+
 struct GatherEngineArgs {
     EngineView v;
-    const SelItem* items;  // the prefetch stream's work list (missed offloaded heads)
+    const SelItem* items;
     const int* count;      // [L]
+    const int32_t* fetch_tok;
+    const int32_t* fetch_slot;
+    const int* fetch_count;
+    int items_cap;
     int layer;
     int count_bytes;
 };
 
+void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream);
 // Row size must be a multiple of 16 bytes (d*sizeof(dtype) % 16 == 0).
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream);
 void launch_gather_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
                       int64_t n_rows, int* err, cudaStream_t stream);
+int reconcile_max_k();
 
 }  // namespace clo

@@ -26,7 +26,9 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     if (a.kind == kKindOffloaded && pers) return;
     if (a.kind == kKindPersistent && !pers) return;
 
-    __shared__ double q[kMaxGroup * kMaxHeadDim];
+    extern __shared__ double dsm[];  // q [m][d], labels [m][d]
+    double* q = dsm;
+    double* lab_s = dsm + v.m * v.d;
     __shared__ double sims[kMaxGroup];
     __shared__ int s_degenerate, s_selected, s_item;
 
@@ -67,13 +69,16 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
         double* lab = v.labels + (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
         int* valid = v.label_valid + ((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m;
         if (threadIdx.x == 0) s_degenerate = 0;
+        // stage the labels in shared memory: the sequential cosine chains then
+        // read smem instead of paying an L2 round trip per element
+        for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab_s[i] = lab[i];
         __syncthreads();
         if (threadIdx.x < v.m) {
             const int j = threadIdx.x;
             sims[j] = 0.0;
             if (valid[j]) {
                 bool deg;
-                const double c = cosine_seq(q + j * v.d, lab + (size_t)j * v.d, v.d, &deg);
+                const double c = cosine_seq(q + j * v.d, lab_s + j * v.d, v.d, &deg);
                 sims[j] = c;
                 if (deg || c <= 0.0) atomicOr(&s_degenerate, 2);
             } else {
@@ -132,7 +137,9 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
             it.rows = v.kmirror ? (const char*)v.kmirror + ((size_t)b * v.NO + v.oidx[lg]) * v.nmax * row_bytes
                                 : nullptr;
         it.codes = v.codes ? v.codes + (size_t)seg * v.nmax * v.words : nullptr;
-        it.out_idx = v.entry_idx + (size_t)seg * v.k;
+        // persistent heads select straight into their entry; offloaded heads
+        // select into scratch and are reconciled with the old entry (delta gather)
+        it.out_idx = pers ? v.entry_idx + (size_t)seg * v.k : a.s.sel + (size_t)item * v.k;
         it.out_score = nullptr;
         a.s.items[item] = it;
     }
@@ -228,7 +235,8 @@ __global__ void aggregate_op_kernel(int n, int m, const double* sims, const doub
 }  // namespace
 
 void launch_prepare(const PrepareArgs& a, cudaStream_t stream) {
-    prepare_kernel<<<a.v.B * a.v.H, kPrepThreads, 0, stream>>>(a);
+    const size_t sm = 2 * (size_t)a.v.m * a.v.d * sizeof(double);
+    prepare_kernel<<<a.v.B * a.v.H, kPrepThreads, sm, stream>>>(a);
 }
 
 void launch_lookup_op(int n_heads, int m, int d, double* labels, int32_t* valid,

@@ -69,11 +69,20 @@ __device__ __forceinline__ void hash_queries_block(const double* q64, int m, int
 #pragma unroll
         for (int j = 0; j < kMaxGroup; ++j) s[j] = 0.0;
         if (b < bits) {
-            for (int c = 0; c < d; ++c) {
-                const double p = proj_t[(size_t)c * bits + b];
+            // P^T loads batched 8 deep so the sequential DADD chains are not
+            // serialised behind one L2 round trip per element
+            for (int c0 = 0; c0 < d; c0 += 8) {
+                double p[8];
 #pragma unroll
-                for (int j = 0; j < kMaxGroup; ++j)
-                    if (j < m) s[j] = dmac(s[j], p, q64[j * d + c]);
+                for (int i = 0; i < 8; ++i) p[i] = c0 + i < d ? proj_t[(size_t)(c0 + i) * bits + b] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (c0 + i < d) {
+#pragma unroll
+                        for (int j = 0; j < kMaxGroup; ++j)
+                            if (j < m) s[j] = dmac(s[j], p[i], q64[j * d + c0 + i]);
+                    }
+                }
             }
         }
 #pragma unroll

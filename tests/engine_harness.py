@@ -92,6 +92,14 @@ def run_and_compare(case, oracle, check_rows=True, tol=None):
     for e, tq, *_ in o_engs:
         e.prefill(tq[0])
     worst = 0.0
+    fetched_rows = 0  # rows the delta gather must move over PCIe (new \ old entry)
+    prev = {}
+    for b in range(len(o_engs)):
+        for l in range(L):
+            for g in range(H):
+                st0 = o_engs[b][0].head_state(l, g)
+                if not st0["persistent"]:
+                    prev[(b, l, g)] = (st0["misses"], set(map(int, st0["entry_indices"])))
     for t in range(1, wl.steps + 1):
         out = g_eng.decode_step()
         for b, (e, tq, aq, nk, nv) in enumerate(o_engs):
@@ -107,6 +115,11 @@ def run_and_compare(case, oracle, check_rows=True, tol=None):
                     assert gs["misses"] == os_["misses"], where
                     assert gs["last_update_step"] == os_["last_update_step"], where
                     if not os_["persistent"]:
+                        pm, pset = prev[(b, l, g)]
+                        cur = set(map(int, os_["entry_indices"]))
+                        if os_["misses"] > pm and cfg.policy == "similarity":
+                            fetched_rows += len(cur - pset)
+                        prev[(b, l, g)] = (os_["misses"], cur)
                         assert gs["window_held_tokens"] == os_["window_held_tokens"], where
                         if cfg.policy == "similarity":
                             np.testing.assert_array_equal(gs["entry_indices"], os_["entry_indices"],
@@ -122,4 +135,8 @@ def run_and_compare(case, oracle, check_rows=True, tol=None):
                                 np.testing.assert_array_equal(widen(vr, cfg.kv_dtype), os_["entry_v"],
                                                               err_msg=where)
     assert worst <= tol, f"worst relative L2 {worst:.3g} > {tol}"
+    if cfg.policy == "similarity":
+        esz = 2 if cfg.kv_dtype == "bf16" else 4
+        got = g_eng.metrics()["gathered_bytes_device"]
+        assert got == fetched_rows * 2 * s.head_dim * esz, (got, fetched_rows)
     return g_eng, o_engs, worst
