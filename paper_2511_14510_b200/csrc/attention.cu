@@ -36,6 +36,9 @@ struct Vec16<float> {
 };
 
 __device__ __forceinline__ float safe_exp2(float x) { return x == -CUDART_INF_F ? 0.f : exp2f(x); }
+// weight of a partial with running max m under the merged max gm; an empty
+// partial (m = -inf) weighs 0 even when gm is -inf too (no NaN)
+__device__ __forceinline__ float wexp(float m, float gm) { return m == -CUDART_INF_F ? 0.f : exp2f(m - gm); }
 
 template <typename T, int D, int M>
 __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v, int l) {
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
             const float om = __shfl_xor_sync(0xffffffffu, mx[j], o);
             const float os = __shfl_xor_sync(0xffffffffu, sm[j], o);
             const float nm = fmaxf(mx[j], om);
-            const float c1 = safe_exp2(mx[j] - nm), c2 = safe_exp2(om - nm);
+            const float c1 = wexp(mx[j], nm), c2 = wexp(om, nm);
             sm[j] = sm[j] * c1 + os * c2;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
         float a = 0.f, s = 0.f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const float cw = safe_exp2(red[w][j][D] - gm);
+            const float cw = wexp(red[w][j][D], gm);
             a += red[w][j][e] * cw;
             s += red[w][j][D + 1] * cw;
         }
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
         for (int cc = 0; cc < nch; ++cc) gm = fmaxf(gm, __ldcg(pb + cc * stride + D));
         float a = 0.f, s = 0.f;
         for (int cc = 0; cc < nch; ++cc) {
-            const float cw = safe_exp2(__ldcg(pb + cc * stride + D) - gm);
+            const float cw = wexp(__ldcg(pb + cc * stride + D), gm);
             a += __ldcg(pb + cc * stride + e) * cw;
             s += __ldcg(pb + cc * stride + D + 1) * cw;
         }

@@ -18,6 +18,10 @@ constexpr int kAttnRows = 256;  // attend positions per CTA (split-K)
 // of each head combines the split partials (no second launch).
 void launch_attention_engine(const EngineView& v, int layer, cudaStream_t stream);
 int attention_chunks(int k, int sink, int recent);
+// TMA-staged production kernel (attention_tma.cu); false = unsupported shape
+// (the caller falls back to launch_attention_engine's register kernel).
+bool attention_tma_supported(int dtype, int d, int m, int k);
+bool launch_attention_tma(const EngineView& v, int layer, cudaStream_t stream);
 bool attention_supported(int dtype, int d, int m);
 
 // Op-level topk_attention for m queries over one matrix (validation separate).

@@ -156,9 +156,9 @@ void Engine::allocate() {
     d_slot_v_.alloc((size_t)B * no_ * k * d * esz);
     d_win_k_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
     d_win_v_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
-    d_entry_idx_.alloc(sizeof(int32_t) * segs * k);
+    d_entry_idx_.alloc(sizeof(int32_t) * segs * k + 64);  // +64: 16-byte rounded token bulk copies
     d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
-    d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k);
+    d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k + 64);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
         d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_, false);
         // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
@@ -643,7 +643,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         launch_append(view(), l, s_main_);
         prof_end(s_main_, "append", l);
         prof_begin(s_main_);
-        launch_attention_engine(view(), l, s_main_);
+        if (!launch_attention_tma(view(), l, s_main_)) launch_attention_engine(view(), l, s_main_);
         prof_end(s_main_, "attention", l);
         launches_ += 2;
         CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));

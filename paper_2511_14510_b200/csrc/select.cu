@@ -184,59 +184,67 @@ __device__ __forceinline__ double key_score<uint64_t>(uint64_t k) { return key_t
 
 // Keeps S > T and the first chunk_take ties S == T (index order) of one chunk,
 // writing indices ascending at chunk_base (select_topk's final ascending sort,
-// retrieval.cpp:43, merge_group_topk's :197-199).
+// retrieval.cpp:43, merge_group_topk's :197-199). Warp w owns 512 consecutive
+// rows: pass 1 counts (coalesced key loads), a tiny 8-warp prefix in shared
+// memory orders the warps, pass 2 re-reads the keys (L1) and emits with
+// ballot/popc ranks — two barriers per chunk, no block-wide scans.
 template <typename KeyT>
 __global__ void __launch_bounds__(kScoreThreads) compact_kernel(SelArgs a) {
-    using Scan = cub::BlockScan<int, kScoreThreads>;
-    __shared__ typename Scan::TempStorage scan_tmp;
+    constexpr int kRowsPerWarp = kScoreChunk / kWarps;  // 512
+    __shared__ int s_gt[kWarps], s_eq[kWarps];
     const int units = *a.count * a.max_chunks;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int item = u / a.max_chunks, chunk = u % a.max_chunks;
         const SelItem it = a.items[item];
         const int start = chunk * kScoreChunk;
         if (start >= it.n) continue;
+        const int end = min(start + kScoreChunk, it.n);
         const KeyT T = (KeyT)a.thresh[item];
         const int take = a.chunk_take[(size_t)item * a.max_chunks + chunk];
         const int base = a.chunk_base[(size_t)item * a.max_chunks + chunk];
         const KeyT* keys = (sizeof(KeyT) == 2 ? (const KeyT*)(a.key16 + (size_t)item * a.nmax)
                                               : (const KeyT*)(a.key64 + (size_t)item * a.nmax));
-        const int r0 = start + threadIdx.x * kRowsPerThread;
-        KeyT kv[kRowsPerThread];
-#pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) {
-            const int r = r0 + i;
-            kv[i] = r < it.n ? keys[r] : (KeyT)0;
+        const int w0 = start + warp * kRowsPerWarp, w1 = min(w0 + kRowsPerWarp, end);
+        int gt = 0, eq = 0;
+        for (int r = w0 + lane; r < w1; r += 32) {
+            const KeyT kv = keys[r];
+            gt += kv > T;
+            eq += kv == T;
         }
-        int n_eq = 0;
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) n_eq += (r0 + i < it.n && kv[i] == T);
-        int eq_prefix;
-        Scan(scan_tmp).ExclusiveSum(n_eq, eq_prefix);
+        for (int o = 16; o > 0; o >>= 1) {
+            gt += __shfl_xor_sync(0xffffffffu, gt, o);
+            eq += __shfl_xor_sync(0xffffffffu, eq, o);
+        }
+        if (lane == 0) {
+            s_gt[warp] = gt;
+            s_eq[warp] = eq;
+        }
         __syncthreads();
-        unsigned selmask = 0;
-        int e = eq_prefix;
-#pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) {
-            if (r0 + i >= it.n) continue;
-            bool s = kv[i] > T;
-            if (kv[i] == T) {
-                s = e < take;
-                ++e;
-            }
-            if (s) selmask |= 1u << i;
+        int eq_before = 0, pos = base;
+        for (int w = 0; w < warp; ++w) {
+            pos += s_gt[w] + max(0, min(s_eq[w], take - eq_before));
+            eq_before += s_eq[w];
         }
-        int pos;
-        Scan(scan_tmp).ExclusiveSum(__popc(selmask), pos);
+        for (int r0 = w0; r0 < w1; r0 += 32) {
+            const int r = r0 + lane;
+            const bool valid = r < w1;
+            const KeyT kv = valid ? keys[r] : (KeyT)0;
+            const bool is_eq = valid && kv == T;
+            const unsigned eqm = __ballot_sync(0xffffffffu, is_eq);
+            const bool sel = (valid && kv > T) || (is_eq && eq_before + __popc(eqm & lt) < take);
+            const unsigned selm = __ballot_sync(0xffffffffu, sel);
+            if (sel) {
+                const int p = pos + __popc(selm & lt);
+                it.out_idx[p] = r;
+                if (it.out_score) it.out_score[p] = key_score<KeyT>(kv);
+            }
+            pos += __popc(selm);
+            eq_before += __popc(eqm);
+        }
         __syncthreads();
-        pos += base;
-#pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) {
-            if (selmask & (1u << i)) {
-                it.out_idx[pos] = r0 + i;
-                if (it.out_score) it.out_score[pos] = key_score<KeyT>(kv[i]);
-                ++pos;
-            }
-        }
     }
 }
 

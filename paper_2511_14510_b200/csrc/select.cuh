@@ -54,20 +54,21 @@ void launch_select_exact(const SelArgs& a, cudaStream_t stream);
 void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, int bits,
                          int words, uint64_t* qbits, cudaStream_t stream);
 
-// Sign bits of m queries (append_sign_row semantics, retrieval.cpp:14-25,
+// Sign bits of M queries (append_sign_row semantics, retrieval.cpp:14-25,
 // as used for the query bits at :113-119): bit b = (sum_c P[b][c]*q[c]) >= 0
 // summed sequentially in IEEE double. Called by a whole CTA (blockDim.x a
-// multiple of 32). q64 [m][d] (smem), proj_t [d][bits] -> qbits [m][words].
-__device__ __forceinline__ void hash_queries_block(const double* q64, int m, int d,
-                                                   const double* proj_t, int bits, int words,
-                                                   uint64_t* qbits_out) {
+// multiple of 32). q64 [M][d] (smem), proj_t [d][bits] -> qbits [M][words].
+// M is a template parameter so no FP64 work is issued for absent members.
+template <int M>
+__device__ __forceinline__ void hash_queries_block_m(const double* q64, int d, const double* proj_t,
+                                                     int bits, int words, uint64_t* qbits_out) {
     uint32_t* out32 = reinterpret_cast<uint32_t*>(qbits_out);
     const int total = words * 64;
     for (int b0 = 0; b0 < total; b0 += blockDim.x) {
         const int b = b0 + threadIdx.x;
-        double s[kMaxGroup];
+        double s[M];
 #pragma unroll
-        for (int j = 0; j < kMaxGroup; ++j) s[j] = 0.0;
+        for (int j = 0; j < M; ++j) s[j] = 0.0;
         if (b < bits) {
             // P^T loads batched 8 deep so the sequential DADD chains are not
             // serialised behind one L2 round trip per element
@@ -79,19 +80,30 @@ __device__ __forceinline__ void hash_queries_block(const double* q64, int m, int
                 for (int i = 0; i < 8; ++i) {
                     if (c0 + i < d) {
 #pragma unroll
-                        for (int j = 0; j < kMaxGroup; ++j)
-                            if (j < m) s[j] = dmac(s[j], p[i], q64[j * d + c0 + i]);
+                        for (int j = 0; j < M; ++j) s[j] = dmac(s[j], p[i], q64[j * d + c0 + i]);
                     }
                 }
             }
         }
 #pragma unroll
-        for (int j = 0; j < kMaxGroup; ++j) {
-            if (j < m) {
-                const unsigned bal = __ballot_sync(0xffffffffu, b < bits && s[j] >= 0.0);
-                if ((threadIdx.x & 31) == 0 && b < total) out32[j * words * 2 + (b >> 5)] = bal;
-            }
+        for (int j = 0; j < M; ++j) {
+            const unsigned bal = __ballot_sync(0xffffffffu, b < bits && s[j] >= 0.0);
+            if ((threadIdx.x & 31) == 0 && b < total) out32[j * words * 2 + (b >> 5)] = bal;
         }
+    }
+}
+
+__device__ __forceinline__ void hash_queries_block(const double* q64, int m, int d,
+                                                   const double* proj_t, int bits, int words,
+                                                   uint64_t* qbits_out) {
+    switch (m) {
+#define CLO_HQ(MM) \
+    case MM: hash_queries_block_m<MM>(q64, d, proj_t, bits, words, qbits_out); return;
+        CLO_HQ(1) CLO_HQ(2) CLO_HQ(3) CLO_HQ(4) CLO_HQ(5) CLO_HQ(6) CLO_HQ(7) CLO_HQ(8)
+#undef CLO_HQ
+        default:
+            for (int j = 0; j < m; ++j)  // large groups: one member at a time
+                hash_queries_block_m<1>(q64 + (size_t)j * d, d, proj_t, bits, words, qbits_out + (size_t)j * words);
     }
 }
 
