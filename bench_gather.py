@@ -1,0 +1,138 @@
+#!/usr/bin/env python3
+"""BASELINE.json configs[4]: zero-copy gather sweep, 256-16384 selected rows per
+head (bf16 K+V rows of d=128 = 256 B each, indices uniform-random distinct
+sorted over n=131072), versus the reference's gather-copy path
+(TransferEngine::kGatherCopy, pipeline_sim.cpp:12-22: CPU threads gather rows
+into a pinned staging buffer, then one cudaMemcpy H2D) and versus the link
+peak (one contiguous pinned cudaMemcpy).
+
+Each measurement moves the K and V rows of `heads` heads in one launch per
+matrix (the engine batches every missed head of a layer the same way).
+Engines: lsu = 16-byte zero-copy loads (the engine's kernel), tma = one
+cp.async.bulk per row from pinned host memory.
+
+  python bench_gather.py [--heads 32] [--reps 5] [--threads 16]
+
+Prints one JSON line per row count, then a summary line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--threads", type=int, default=min(16, os.cpu_count() or 1))
+    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--rows", default="256,512,1024,2048,4096,8192,16384")
+    ap.add_argument("--ctas", type=int, default=0)
+    args = ap.parse_args()
+
+    import torch
+    from paper_2511_14510_b200 import _lib
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    d, esz, n, H = 128, 2, args.n, args.heads
+    row_bytes = d * esz
+    # host store: H heads x n rows, K and V, pinned + mapped
+    nbytes = H * n * row_bytes
+    ptrs = []
+    for _ in range(2):
+        p = C.c_void_p()
+        _lib.check(lib.clo_host_alloc(nbytes, C.byref(p)))
+        ptrs.append(p.value)
+        arr = np.frombuffer((C.c_char * nbytes).from_address(p.value), dtype=np.uint16)
+        arr[:] = np.random.default_rng(len(ptrs)).integers(0, 65535, arr.size, dtype=np.uint16)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    # link peak: contiguous pinned memcpy of 1 GiB
+    pin = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    dbuf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    peak = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dbuf.copy_(pin, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        peak = max(peak, (1 << 30) / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del pin, dbuf
+
+    rng = np.random.default_rng(7)
+    results = []
+    for r in [int(x) for x in args.rows.split(",")]:
+        idx = np.concatenate([np.sort(rng.choice(n, r, replace=False)) + h * n for h in range(H)]).astype(np.int32)
+        didx = torch.from_numpy(idx).to(dev)
+        dst = torch.empty((2, H * r, d), dtype=torch.int16, device=dev)
+        moved = 2 * H * r * row_bytes
+        line = {"rows_per_head": r, "heads": H, "bytes": moved}
+        for name, engine in (("lsu", 0), ("tma", 1)):
+            best = None
+            for rep in range(args.reps + 1):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for m in range(2):
+                    _lib.check(lib.clo_gather_rows_ex(ptrs[m], _lib.DTYPE_BF16, d, H * n, didx.data_ptr(), H * r,
+                                                      dst[m].data_ptr(), engine, args.ctas, err.data_ptr(), sp))
+                b.record(stream)
+                torch.cuda.synchronize()
+                if rep:
+                    ms = a.elapsed_time(b)
+                    best = ms if best is None else min(best, ms)
+            assert int(err.item()) == 0
+            # bit-exact check against the host rows
+            hk = np.frombuffer((C.c_char * nbytes).from_address(ptrs[0]), dtype=np.uint16).reshape(H * n, d)
+            got = dst[0].cpu().numpy().view(np.uint16)
+            sample = np.arange(0, H * r, max(1, (H * r) // 257))
+            assert np.array_equal(got[sample], hk[idx[sample]]), name
+            line[f"{name}_ms"] = best
+            line[f"{name}_gbs"] = moved / (best * 1e-3) / 1e9
+        # gather-copy baseline: CPU threads gather into pinned staging, then H2D
+        stg = C.c_void_p()
+        _lib.check(lib.clo_host_alloc(H * r * row_bytes, C.byref(stg)))
+        hidx = np.ascontiguousarray(idx)
+        best = None
+        for rep in range(min(args.reps, 3) + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for m in range(2):
+                _lib.check(lib.clo_gather_rows_cpu_staged(ptrs[m], _lib.DTYPE_BF16, d, H * n, hidx.ctypes.data, H * r,
+                                                          stg.value, dst[m].data_ptr(), args.threads, sp))
+                torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            if rep:
+                best = el if best is None else min(best, el)
+        lib.clo_host_free(stg.value)
+        line["cpu_staged_ms"] = best * 1e3
+        line["cpu_staged_gbs"] = moved / best / 1e9
+        line["cpu_threads"] = args.threads
+        line["link_peak_gbs"] = peak
+        line["lsu_frac_of_peak"] = line["lsu_gbs"] / peak
+        line["tma_frac_of_peak"] = line["tma_gbs"] / peak
+        results.append(line)
+        print(json.dumps(line), flush=True)
+    for p in ptrs:
+        lib.clo_host_free(p)
+    print(json.dumps({"summary": "zero-copy gather sweep (configs[4]), 1 GPU",
+                      "link_peak_gbs_pinned_memcpy": peak, "pcie_gen5_x16_theoretical_gbs": 64.0,
+                      "best_lsu_gbs": max(x["lsu_gbs"] for x in results),
+                      "best_tma_gbs": max(x["tma_gbs"] for x in results),
+                      "best_cpu_staged_gbs": max(x["cpu_staged_gbs"] for x in results)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

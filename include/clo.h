@@ -306,6 +306,14 @@ clo_status clo_gather_rows(const void* src, int dtype, int d, int64_t n_rows,
 /* Gather-copy baseline (TransferEngine::kGatherCopy, pipeline_sim.cpp:12-22):
  * `threads` CPU threads gather rows into a pinned staging buffer, then one
  * cudaMemcpyAsync H2D. idx_host [k]. */
+/* Asynchronous variant for benchmarking the transfer engines: engine 0 = LSU
+ * zero-copy gather (16-byte loads), 1 = TMA bulk-copy gather (one
+ * cp.async.bulk per row from pinned host memory). `ctas` caps the grid
+ * (<= 0: default). Index errors are OR'ed into *err_dev; no synchronisation. */
+clo_status clo_gather_rows_ex(const void* src, int dtype, int d, int64_t n_rows,
+                              const int32_t* idx_dev, int k, void* dst_dev, int engine, int ctas,
+                              int* err_dev, void* stream);
+
 clo_status clo_gather_rows_cpu_staged(const void* src_host, int dtype, int d, int64_t n_rows,
                                       const int32_t* idx_host, int k, void* staging_host,
                                       void* dst_dev, int threads, void* stream);

@@ -153,6 +153,7 @@ SIGNATURES = {
     "clo_cosine_similarity": (_I, [_I, _I, _P, _P, _P, _P, _P]),
     "clo_aggregate_similarity": (_I, [_I, _I, _P, _P, _P, _P]),
     "clo_gather_rows": (_I, [_P, _I, _I, _I64, _P, _I, _P, _P]),
+    "clo_gather_rows_ex": (_I, [_P, _I, _I, _I64, _P, _I, _P, _I, _I, _P, _P]),
     "clo_gather_rows_cpu_staged": (_I, [_P, _I, _I, _I64, _P, _I, _P, _P, _I, _P]),
     "clo_topk_attention": (_I, [_P, _I, _P, _P, _I, _I64, _I, _P, _I, _P, _P]),
     "clo_sink_recent_indices": (_I, [_I, _I, _I, _P, C.POINTER(_I), C.POINTER(_I)]),

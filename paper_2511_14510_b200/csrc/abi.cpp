@@ -458,9 +458,26 @@ clo_status clo_gather_rows(const void* src, int dtype, int d, int64_t n_rows,
         if (k < 0) fail(CLO_ERR_ARGUMENT, "negative row count");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         OpErr err;
-        if (k > 0) launch_gather_op(src, dst_dev, idx_dev, row_bytes, k, n_rows, err.ptr(), s);
+        if (k > 0) launch_gather_op(src, dst_dev, idx_dev, row_bytes, k, n_rows, err.ptr(), 0, s);
         CLO_CUDA(cudaGetLastError());
         if (err.read(s) & kErrIndexRange) fail(CLO_ERR_INDEX, "matrix row out of range");
+    });
+}
+
+clo_status clo_gather_rows_ex(const void* src, int dtype, int d, int64_t n_rows,
+                              const int32_t* idx_dev, int k, void* dst_dev, int engine, int ctas,
+                              int* err_dev, void* stream) {
+    return guarded([&] {
+        const int row_bytes = d * dsize(dtype);
+        if (row_bytes % 16 != 0) fail(CLO_ERR_SHAPE, "rows must be a multiple of 16 bytes");
+        if (!err_dev) fail(CLO_ERR_ARGUMENT, "err_dev must be a device int");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (k <= 0) return;
+        if (engine == 1)
+            launch_gather_tma_op(src, dst_dev, idx_dev, row_bytes, k, n_rows, err_dev, ctas > 0 ? ctas : 64, s);
+        else
+            launch_gather_op(src, dst_dev, idx_dev, row_bytes, k, n_rows, err_dev, ctas, s);
+        CLO_CUDA(cudaGetLastError());
     });
 }
 

@@ -201,7 +201,99 @@ __global__ void __launch_bounds__(kGatherThreads) gather_op_kernel(const uint4* 
     }
 }
 
+// ---------------------------------------------------------- TMA bulk gather
+// Same copy, driven by the TMA unit instead of LSU loads: one 1D bulk copy
+// (cp.async.bulk global->shared) per row straight out of pinned host memory
+// into a shared-memory stage, completion on an mbarrier, then one bulk store
+// of the 32-row stage to its contiguous destination. One warp per CTA keeps
+// kTmaStages x 32 rows in flight without holding registers.
+constexpr int kTmaStages = 4;
+constexpr int kTmaRows = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32) gather_tma_kernel(const char* __restrict__ src, char* __restrict__ dst,
+                                                        const int32_t* __restrict__ idx, int row_bytes, int k,
+                                                        int64_t n_rows, int* err) {
+    extern __shared__ __align__(128) char stage[];  // [kTmaStages][kTmaRows][row_bytes]
+    __shared__ __align__(8) uint64_t bar[kTmaStages];
+    const int lane = threadIdx.x;
+    const int groups = (k + kTmaRows - 1) / kTmaRows;
+    if (lane == 0) {
+        for (int s = 0; s < kTmaStages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // this CTA's groups: blockIdx.x, blockIdx.x + gridDim.x, ...
+    const int mine = groups > (int)blockIdx.x ? (groups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto load = [&](int i) {  // i-th group of this CTA into stage i % S
+        const int g = blockIdx.x + i * gridDim.x;
+        const int s = i % kTmaStages;
+        const int rows = min(kTmaRows, k - g * kTmaRows);
+        char* st = stage + (size_t)s * kTmaRows * row_bytes;
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])),
+                         "r"(rows * row_bytes)
+                         : "memory");
+        }
+        __syncwarp();
+        if (lane < rows) {
+            int32_t ix = idx[g * kTmaRows + lane];
+            if (ix < 0 || ix >= n_rows) {
+                atomicOr(err, kErrIndexRange);
+                ix = 0;
+            }
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(st + (size_t)lane * row_bytes)),
+                "l"(src + (size_t)ix * row_bytes), "r"(row_bytes), "r"(smem_u32(&bar[s]))
+                : "memory");
+        }
+    };
+    for (int i = 0; i < min(kTmaStages, mine); ++i) load(i);
+    for (int i = 0; i < mine; ++i) {
+        const int g = blockIdx.x + i * gridDim.x;
+        const int s = i % kTmaStages;
+        const int rows = min(kTmaRows, k - g * kTmaRows);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra W_%=;\n\t}" ::"r"(smem_u32(&bar[s])),
+            "r"((i / kTmaStages) & 1)
+            : "memory");
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                             dst + (size_t)g * kTmaRows * row_bytes),
+                         "r"(smem_u32(stage + (size_t)s * kTmaRows * row_bytes)), "r"(rows * row_bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage reusable
+        }
+        __syncwarp();
+        if (i + kTmaStages < mine) load(i + kTmaStages);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
+
+void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
+                          int64_t n_rows, int* err, int ctas, cudaStream_t stream) {
+    const int groups = (k + kTmaRows - 1) / kTmaRows;
+    const int grid = groups < ctas ? (groups > 0 ? groups : 1) : ctas;
+    const size_t sm = (size_t)kTmaStages * kTmaRows * row_bytes;
+    static size_t configured = 0;
+    if (sm > 48 * 1024 && sm > configured) {
+        cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        configured = sm;
+    }
+    gather_tma_kernel<<<grid, 32, sm, stream>>>(static_cast<const char*>(src), static_cast<char*>(dst), idx,
+                                                 row_bytes, k, n_rows, err);
+}
 
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
     const size_t sm = sizeof(int32_t) * 4 * (size_t)a.v.k;
@@ -216,10 +308,11 @@ void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stre
 }
 
 void launch_gather_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
-                      int64_t n_rows, int* err, cudaStream_t stream) {
+                      int64_t n_rows, int* err, int ctas, cudaStream_t stream) {
     const int vpr = row_bytes / 16;
     const int units = (k * vpr + kVecsPerUnit - 1) / kVecsPerUnit;
-    const int grid = units < kNumSMs * 8 ? (units > 0 ? units : 1) : kNumSMs * 8;
+    const int cap = ctas > 0 ? ctas : kNumSMs * 8;
+    const int grid = units < cap ? (units > 0 ? units : 1) : cap;
     gather_op_kernel<<<grid, kGatherThreads, 0, stream>>>(static_cast<const uint4*>(src),
                                                           static_cast<uint4*>(dst), idx, vpr, k,
                                                           n_rows, err);

@@ -35,8 +35,11 @@ struct GatherEngineArgs {
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream);
 // Row size must be a multiple of 16 bytes (d*sizeof(dtype) % 16 == 0).
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream);
+// ctas <= 0: default grid
 void launch_gather_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
-                      int64_t n_rows, int* err, cudaStream_t stream);
+                      int64_t n_rows, int* err, int ctas, cudaStream_t stream);
+void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
+                          int64_t n_rows, int* err, int ctas, cudaStream_t stream);
 int reconcile_max_k();
 
 }  // namespace clo
