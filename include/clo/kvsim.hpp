@@ -1,0 +1,228 @@
+// clo/kvsim.hpp — header-only C++ shim that re-exposes the reference's kvsim
+// API names (engine.hpp, retrieval.hpp, similarity_cache.hpp, attention.hpp,
+// head_profile.hpp, errors.hpp) over the C-ABI in <clo.h>, so runner-style
+// callers written against kvsim compile against the B200 library by swapping
+// the include and the namespace.
+//
+// Status codes are rethrown as the matching exception type (errors.hpp:10-41).
+#pragma once
+
+#include <clo.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace clo::kvsim {
+
+// ---- errors.hpp:10-41 -----------------------------------------------------
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error { using Error::Error; };
+struct ArgumentError : Error { using Error::Error; };
+struct NumericError : Error { using Error::Error; };
+struct IndexError : Error { using Error::Error; };
+struct ContractError : Error { using Error::Error; };
+struct ConfigError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct CudaError : Error { using Error::Error; };
+
+inline void check(clo_status s) {
+    if (s == CLO_OK) return;
+    const std::string m = clo_last_error();
+    switch (s) {
+        case CLO_ERR_SHAPE: throw ShapeError(m);
+        case CLO_ERR_ARGUMENT: throw ArgumentError(m);
+        case CLO_ERR_NUMERIC: throw NumericError(m);
+        case CLO_ERR_INDEX: throw IndexError(m);
+        case CLO_ERR_CONTRACT: throw ContractError(m);
+        case CLO_ERR_CONFIG: throw ConfigError(m);
+        case CLO_ERR_IO: throw IoError(m);
+        case CLO_ERR_CUDA: throw CudaError(m);
+        default: throw Error(m);
+    }
+}
+
+// ---- matrix.hpp:46-66 / engine.hpp:19-49 ------------------------------------
+using ModelShape = clo_model_shape;
+enum class Policy { kSimilarity = CLO_POLICY_SIMILARITY, kLru = CLO_POLICY_LRU, kLfu = CLO_POLICY_LFU,
+                    kPrefetchOnly = CLO_POLICY_PREFETCH_ONLY };
+enum class RetrieverVariant { kExact = CLO_RETRIEVER_EXACT, kSignHash = CLO_RETRIEVER_SIGN_HASH };
+enum class SyncMode { kCpuCentric = CLO_SYNC_CPU_CENTRIC, kGpuCentric = CLO_SYNC_GPU_CENTRIC };
+enum class Placement { kOffloaded = CLO_PLACEMENT_OFFLOADED, kPersistent = CLO_PLACEMENT_PERSISTENT };
+
+struct ModeFlags {
+    bool always_miss = false;
+    bool always_hit = false;
+    std::optional<double> tau_override;
+};
+
+struct EngineConfig {
+    ModelShape shape{};
+    int k = 0;
+    int sink_tokens = 4;
+    int recent_tokens = 64;
+    RetrieverVariant retriever = RetrieverVariant::kExact;
+    int hash_bits = 256;
+    uint64_t retriever_seed = 1;
+    Policy policy = Policy::kSimilarity;
+    ModeFlags mode;
+    std::optional<SyncMode> sync_override;
+    bool collect_outputs = false;
+    bool compute_oracle_error = false;
+    // B200
+    int batch = 1;
+    int kv_dtype = CLO_DTYPE_BF16;
+    int kv_head_offset = 0;
+    int device = 0;
+
+    clo_engine_config to_c(int n_prompt, int max_steps) const {
+        clo_engine_config c;
+        clo_engine_config_defaults(&c);
+        c.shape = shape;
+        c.k = k;
+        c.sink_tokens = sink_tokens;
+        c.recent_tokens = recent_tokens;
+        c.retriever = static_cast<int>(retriever);
+        c.hash_bits = hash_bits;
+        c.retriever_seed = retriever_seed;
+        c.policy = static_cast<int>(policy);
+        c.always_miss = mode.always_miss;
+        c.always_hit = mode.always_hit;
+        c.has_tau_override = mode.tau_override.has_value();
+        c.tau_override = mode.tau_override.value_or(0.0);
+        c.sync_override = sync_override ? static_cast<int>(*sync_override) : -1;
+        c.collect_outputs = collect_outputs;
+        c.compute_oracle_error = compute_oracle_error;
+        c.batch = batch;
+        c.n_prompt = n_prompt;
+        c.max_steps = max_steps;
+        c.kv_dtype = kv_dtype;
+        c.kv_head_offset = kv_head_offset;
+        c.device = device;
+        return c;
+    }
+};
+
+// head_profile.hpp:16-23, 85-97
+struct HeadProfileEntry {
+    std::vector<double> q_importance;
+    double kv_importance = 0.0;
+    double s_hat = 0.0;
+    double tau = -1.0;
+    double difficulty = 0.0;
+    Placement placement = Placement::kOffloaded;
+};
+using HeadProfiles = std::vector<std::vector<HeadProfileEntry>>;
+struct LayerPartition {
+    int n_d = 0;
+    int n_persist = 0;
+    std::vector<int> persistent_heads;
+};
+struct PartitionPlan {
+    int n_p = 0;
+    std::vector<LayerPartition> layers;
+};
+
+// ---- DecodeEngine (engine.hpp:91-139) -------------------------------------
+// The StepSource is replaced by explicit per-step inputs (device or host
+// buffers), since the step data lives on the GPU.
+class DecodeEngine {
+  public:
+    DecodeEngine(const EngineConfig& cfg, const HeadProfiles& profiles, const PartitionPlan& plan,
+                 int n_prompt, int decode_steps)
+        : cfg_(cfg) {
+        const int L = cfg.shape.num_layers, H = cfg.shape.num_kv_heads;
+        const int m = cfg.shape.num_kv_heads ? cfg.shape.num_q_heads / cfg.shape.num_kv_heads : 0;
+        if (static_cast<int>(profiles.size()) != L) throw ArgumentError("profiles must cover every layer");
+        if (static_cast<int>(plan.layers.size()) != L) throw ArgumentError("partition plan must cover every layer");
+        std::vector<double> tau, qimp;
+        std::vector<int> pers(static_cast<size_t>(L) * H, 0);
+        for (int l = 0; l < L; ++l) {
+            if (static_cast<int>(profiles[l].size()) != H) throw ArgumentError("profiles must cover every KV head");
+            for (const auto& e : profiles[l]) {
+                if (static_cast<int>(e.q_importance.size()) != m)
+                    throw ArgumentError("profile importance width must equal the group size");
+                tau.push_back(e.tau);
+                qimp.insert(qimp.end(), e.q_importance.begin(), e.q_importance.end());
+            }
+            for (int g : plan.layers[l].persistent_heads) {
+                if (g < 0 || g >= H) throw ArgumentError("partition plan names a KV head outside the model");
+                pers[static_cast<size_t>(l) * H + g] = 1;
+            }
+        }
+        const clo_engine_config c = cfg.to_c(n_prompt, decode_steps);
+        check(clo_engine_create(&c, tau.data(), qimp.data(), pers.data(), &e_));
+    }
+    ~DecodeEngine() { clo_engine_destroy(e_); }
+    DecodeEngine(const DecodeEngine&) = delete;
+    DecodeEngine& operator=(const DecodeEngine&) = delete;
+
+    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride) {
+        check(clo_engine_bind_host_kv(e_, k, v, seq_stride, layer_stride, head_stride));
+    }
+    void prefill(const float* true_q0, bool on_host = true, void* stream = nullptr) {
+        check(clo_prefill(e_, true_q0, on_host, stream));
+    }
+    void decode_step(const clo_step_io& io, void* stream = nullptr) { check(clo_decode_step(e_, &io, stream)); }
+    clo_metrics metrics() const {
+        clo_metrics m;
+        check(clo_get_metrics(e_, &m));
+        return m;
+    }
+    SyncMode sync_mode() const { return static_cast<SyncMode>(metrics().sync_mode); }
+    uint64_t host_bytes() const { return metrics().host_bytes; }
+    uint64_t device_persistent_bytes() const { return metrics().device_persistent_bytes; }
+    uint64_t modeled_cache_bytes() const { return metrics().cache_bytes_current; }
+    clo_head_state head(int layer, int kv_head, int seq = 0, std::vector<int32_t>* entry = nullptr,
+                        std::vector<double>* history = nullptr) const {
+        clo_head_state st;
+        if (entry) entry->resize(cfg_.k);
+        if (history) history->resize(1u << 16);
+        check(clo_get_head_state(e_, seq, layer, kv_head, &st, entry ? entry->data() : nullptr,
+                                 history ? history->data() : nullptr));
+        if (history) history->resize(st.n_history);
+        return st;
+    }
+    std::string cache_state_json(int seq = 0) const {
+        size_t need = 0;
+        check(clo_cache_state_json(e_, seq, nullptr, 0, &need));
+        std::string s(need, '\0');
+        check(clo_cache_state_json(e_, seq, s.data(), need, &need));
+        s.resize(need ? need - 1 : 0);
+        return s;
+    }
+    clo_engine* handle() const { return e_; }
+
+  private:
+    EngineConfig cfg_;
+    clo_engine* e_ = nullptr;
+};
+
+// ---- pure functions ---------------------------------------------------------
+inline double compute_threshold(double s, double eta, double p) {  // head_profile.cpp:17-25
+    double tau;
+    check(clo_compute_threshold(s, eta, p, &tau));
+    return tau;
+}
+inline double compute_difficulty(double tau, double s_hat, double epsilon) {
+    double d;
+    check(clo_compute_difficulty(tau, s_hat, epsilon, &d));
+    return d;
+}
+inline std::vector<int> sink_recent_indices(int n, int sink, int recent, bool* clamped = nullptr) {
+    std::vector<int32_t> out(static_cast<size_t>(std::max(0, std::min(n, sink)) + std::max(0, std::min(n, recent))) + 1);
+    int count = 0, cl = 0;
+    check(clo_sink_recent_indices(n, sink, recent, out.data(), &count, &cl));
+    if (clamped) *clamped = cl;
+    return {out.begin(), out.begin() + count};
+}
+inline uint64_t cache_bytes(int offloaded, int entry_k, int held, int L, int hq, int d, int e) {
+    return clo_cache_bytes(offloaded, entry_k, held, L, hq, d, e);
+}
+
+}  // namespace clo::kvsim

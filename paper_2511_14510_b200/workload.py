@@ -129,3 +129,21 @@ def synthetic_profiles(shape: Shape, seed: int = 7, eta: float = 0.8, p: float =
         for g in range(H):
             tau[l, g] = threshold(float(qimp[l, g].max()), eta, p)
     return tau, qimp
+
+
+class HeadSlice:
+    """View of a SyntheticWorkload restricted to KV heads [kv0, kv0+n_kv) and
+    their query heads (a KV-head shard, paper_2511_14510_b200/dist.py)."""
+
+    def __init__(self, wl: SyntheticWorkload, kv0: int, n_kv: int, q0: int, n_q: int):
+        self.shape = Shape(wl.shape.num_layers, n_q, n_kv, wl.shape.head_dim)
+        self.batch, self.n_prompt, self.steps = wl.batch, wl.n_prompt, wl.steps
+        self.kv_dtype, self.alias_layers = wl.kv_dtype, wl.alias_layers
+        self.prompt_k = np.ascontiguousarray(wl.prompt_k[:, :, kv0:kv0 + n_kv])
+        self.prompt_v = np.ascontiguousarray(wl.prompt_v[:, :, kv0:kv0 + n_kv])
+        self.new_k = np.ascontiguousarray(wl.new_k[:, :, :, kv0:kv0 + n_kv])
+        self.new_v = np.ascontiguousarray(wl.new_v[:, :, :, kv0:kv0 + n_kv])
+        self.true_q = np.ascontiguousarray(wl.true_q[:, :, :, q0:q0 + n_q])
+        self.approx_q = np.ascontiguousarray(wl.approx_q[:, :, :, q0:q0 + n_q])
+
+    step_new_kv = SyntheticWorkload.step_new_kv

@@ -115,3 +115,24 @@ def test_engine_without_device_fails_loudly(clo):
     h = C.c_void_p()
     st = clo.clo_engine_create(C.byref(c), tau.ctypes.data, qi.ctypes.data, pers.ctypes.data, C.byref(h))
     assert st == 8  # CLO_ERR_CUDA
+
+
+def test_cpp_shim_compiles_links_and_runs(tmp_path):
+    """include/clo/kvsim.hpp: a kvsim-style C++ caller builds against the
+    library and gets the reference's exception types (tests/cpp/shim_check.cpp)."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("no C++ compiler")
+    exe = tmp_path / "shim_check"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "shim_check.cpp"), "-L", libdir, "-lclo",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except ImportError:
+        gpu = False
+    r = subprocess.run([str(exe)] + (["gpu"] if gpu else []), capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
