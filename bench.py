@@ -309,12 +309,15 @@ def run_ours(args):
     launches0 = eng.kernel_launches()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     with ClockSampler(local) as clocks:
         ev0.record(stream)
-        for _ in range(K):
+        for i in range(K):
             step_dev()
+            step_ev[i].record(stream)
         ev1.record(stream)
         barrier()
+    step_ms = [ev0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, K)]
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = eng.kernel_launches() - launches0
     m1 = eng.metrics()
@@ -444,6 +447,7 @@ def run_ours(args):
                        "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers",
                        "sigma_step": args.sigma, "sigma_layer": args.sigma_layer},
             "hit_ratio": hits / max(1, hits + misses),
+            "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms), "max": max(step_ms)},
             "pcie_gather_gbs_in_step": gathered / (ms / 1e3) / 1e9,
             "pcie_link_peak_gbs": best,
             "per_kernel_ms": {kk: round(v["ms"], 4) for kk, v in sorted(per_kernel.items())},

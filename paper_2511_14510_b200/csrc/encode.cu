@@ -106,12 +106,12 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
             const int bit = b0 + threadIdx.x;
             double s = 0.0;
             if (bit < v.bits)
-                for (int c0 = 0; c0 < v.d; c0 += 8) {  // batched loads, sequential chain
-                    double p[8];
+                for (int c0 = 0; c0 < v.d; c0 += 32) {  // 32 loads in flight, sequential chain
+                    double p[32];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) p[i] = c0 + i < v.d ? pt[(size_t)(c0 + i) * v.bits + bit] : 0.0;
+                    for (int i = 0; i < 32; ++i) p[i] = c0 + i < v.d ? pt[(size_t)(c0 + i) * v.bits + bit] : 0.0;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < 32; ++i)
                         if (c0 + i < v.d) s = dmac(s, p[i], kd[c0 + i]);
                 }
             const unsigned bal = __ballot_sync(0xffffffffu, bit < v.bits && s >= 0.0);

@@ -249,7 +249,12 @@ void Engine::allocate() {
 
     CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
     CLO_CUDA(cudaStreamCreateWithFlags(&s_pref_, cudaStreamNonBlocking));
-    CLO_CUDA(cudaStreamCreateWithFlags(&s_xfer_, cudaStreamNonBlocking));
+    // The transfer stream gets the highest priority: when attention CTAs
+    // retire, the next layer's gather CTAs are scheduled first so the PCIe
+    // link does not idle behind compute.
+    int prio_lo = 0, prio_hi = 0;
+    CLO_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CLO_CUDA(cudaStreamCreateWithPriority(&s_xfer_, cudaStreamNonBlocking, prio_hi));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));

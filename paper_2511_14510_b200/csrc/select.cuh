@@ -70,14 +70,14 @@ __device__ __forceinline__ void hash_queries_block_m(const double* q64, int d, c
 #pragma unroll
         for (int j = 0; j < M; ++j) s[j] = 0.0;
         if (b < bits) {
-            // P^T loads batched 8 deep so the sequential DADD chains are not
+            // P^T loads batched 32 deep so the sequential DADD chains are not
             // serialised behind one L2 round trip per element
-            for (int c0 = 0; c0 < d; c0 += 8) {
-                double p[8];
+            for (int c0 = 0; c0 < d; c0 += 32) {
+                double p[32];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) p[i] = c0 + i < d ? proj_t[(size_t)(c0 + i) * bits + b] : 0.0;
+                for (int i = 0; i < 32; ++i) p[i] = c0 + i < d ? proj_t[(size_t)(c0 + i) * bits + b] : 0.0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < 32; ++i) {
                     if (c0 + i < d) {
 #pragma unroll
                         for (int j = 0; j < M; ++j) s[j] = dmac(s[j], p[i], q64[j * d + c0 + i]);
