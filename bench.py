@@ -37,7 +37,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG2 = dict(layers=32, q_heads=32, kv_heads=8, head_dim=128, batch=16, ctx=131072, k=2048)
+# BASELINE.json configs, 1-based as in SURVEY.md §8d. configs[1] (= 2 here) is
+# the headline the metric is quoted on and the default.
+CONFIGS = {
+    1: dict(name="configs[0]: single decode step, Llama-3-8B attention (32q/8kv, d128), batch 1, 32K ctx, "
+                 "top-k 2048, cold gather of every offloaded head (always_miss)",
+            layers=32, q_heads=32, kv_heads=8, head_dim=128, batch=1, ctx=32768, k=2048,
+            always_miss=True, plan="layer0", shard="requests"),
+    2: dict(name="configs[1]: Llama-3.1-8B attention shape (32 layers, 32q/8kv, d128), batch 16 per GPU, "
+                 "128K ctx, top-k 2048, head-wise cache + prefetch, sign-hash 256b, layer 0 persistent",
+            layers=32, q_heads=32, kv_heads=8, head_dim=128, batch=16, ctx=131072, k=2048,
+            always_miss=False, plan="layer0", shard="requests"),
+    3: dict(name="configs[2]: Qwen2.5-14B-Instruct-1M attention (48 layers, 40q/8kv, d128), batch 4, 512K ctx, "
+                 "top-k 2048, persistent hard heads from plan_partition",
+            layers=48, q_heads=40, kv_heads=8, head_dim=128, batch=4, ctx=524288, k=2048,
+            always_miss=False, plan="partition", shard="requests"),
+    4: dict(name="configs[3]: Llama-3.1-8B attention, 1M ctx, batch 8, KV heads sharded across GPUs "
+                 "(per-GPU PCIe zero-copy, NCCL head-output all-gather)",
+            layers=32, q_heads=32, kv_heads=8, head_dim=128, batch=8, ctx=1048576, k=2048,
+            always_miss=False, plan="layer0", shard="heads"),
+}
+CONFIG2 = CONFIGS[2]
 METRIC = "decode tokens/s @128K ctx (1/2/4/8 GPU); zero-copy PCIe GB/s vs link peak"
 
 
@@ -47,16 +67,22 @@ def parse():
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=CONFIG2["batch"])
-    ap.add_argument("--ctx", type=int, default=CONFIG2["ctx"])
-    ap.add_argument("--layers", type=int, default=CONFIG2["layers"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch")
+    ap.add_argument("--ctx", type=int, default=0, help="override the config's context")
+    ap.add_argument("--layers", type=int, default=0, help="override the config's layer count")
     ap.add_argument("--sigma", type=float, default=0.05, help="query drift per decode step")
     ap.add_argument("--sigma-layer", type=float, default=0.01)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
-    return ap.parse_args()
+    args = ap.parse_args()
+    args.cfg = dict(CONFIGS[args.config])
+    args.batch = args.batch or args.cfg["batch"]
+    args.ctx = args.ctx or args.cfg["ctx"]
+    args.layers = args.layers or args.cfg["layers"]
+    return args
 
 
 # --------------------------------------------------------------------- helpers
@@ -127,7 +153,8 @@ def reference_sample(args, steps: int, warmup: int, threads: int):
     C restatement ('port') when the reference library is absent."""
     from oracle.bind import EngineCfg, Oracle, Reference
     from paper_2511_14510_b200.workload import _normalize
-    d, m, n = CONFIG2["head_dim"], CONFIG2["q_heads"] // CONFIG2["kv_heads"], args.ctx
+    C2 = args.cfg
+    d, m, n = C2["head_dim"], C2["q_heads"] // C2["kv_heads"], args.ctx
     rng = np.random.default_rng(args.seed)
     bf = lambda a: ((a.astype(np.float32).view(np.uint32) + 0x8000) & 0xFFFF0000).view(np.float32)
     pk = bf(rng.standard_normal((1, 1, n, d), np.float32)).astype(np.float64)
@@ -145,7 +172,8 @@ def reference_sample(args, steps: int, warmup: int, threads: int):
     qimp = rng.uniform(0, 1, m)
     c = EngineCfg()
     c.num_layers, c.num_q_heads, c.num_kv_heads, c.head_dim, c.bytes_per_element = 1, m, 1, d, 2
-    c.k, c.sink_tokens, c.recent_tokens = CONFIG2["k"], 4, 64
+    c.k, c.sink_tokens, c.recent_tokens = C2["k"], 4, 64
+    c.always_miss = int(C2["always_miss"])
     c.retriever, c.hash_bits, c.retriever_seed, c.policy = 1, 256, 1, 0
     c.n_prompt, c.steps = n, steps
     tau = 0.3
@@ -169,24 +197,38 @@ def reference_sample(args, steps: int, warmup: int, threads: int):
         per_unit = (time.perf_counter() - ts) / max(1, steps - warmup)
         threads = 1
     wall = time.time() - t0
-    units_per_token_step = args.batch * args.layers * CONFIG2["kv_heads"]
+    units_per_token_step = args.batch * args.layers * C2["kv_heads"]
     # `threads` units run concurrently; one decode step of the whole batch needs
     # units_per_token_step units, producing `batch` tokens.
     tokens_per_s = args.batch * threads / (units_per_token_step * per_unit)
     sample = (f"{threads} concurrent reference DecodeEngines, each one (sequence, layer, KV head) "
-              f"unit at ctx={n}, m={m}, k={CONFIG2['k']}, sign-hash, similarity policy, "
+              f"unit at ctx={n}, m={m}, k={C2['k']}, sign-hash, similarity policy"
+              f"{' (always_miss)' if C2['always_miss'] else ''}, "
               f"{steps - warmup} timed decode_steps after {warmup} warm-up; {per_unit * 1e3:.1f} ms "
               f"per unit-step; extrapolated x{units_per_token_step} units per batch step "
-              f"(B={args.batch}, L={args.layers}, H={CONFIG2['kv_heads']}); wall {wall:.1f}s")
+              f"(B={args.batch}, L={args.layers}, H={C2['kv_heads']}); wall {wall:.1f}s")
     return {"value": tokens_per_s, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
             "sec_per_unit_step": per_unit}
+
+
+def cpu_threads(args):
+    """All host threads, capped so the per-thread reference engines (about four
+    n x d double matrices each) stay within half of the host RAM."""
+    threads = args.cpu_threads or os.cpu_count() or 1
+    try:
+        import psutil
+        ram = psutil.virtual_memory().total
+    except ImportError:
+        ram = 64 << 30
+    per_thread = 4 * args.ctx * args.cfg["head_dim"] * 8 + (1 << 28)
+    return max(1, min(threads, int(0.5 * ram // per_thread)))
 
 
 def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    threads = args.cpu_threads or os.cpu_count() or 1
+    threads = cpu_threads(args)
     steps = args.warmup + args.steps
     # bound the sample: at 128K each unit-step costs ~0.2 s of CPU
     steps = min(steps, args.warmup + 8)
@@ -196,8 +238,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": steps - min(args.warmup, 1), "warmup": min(args.warmup, 1),
         "ms_per_step": 1e3 * args.batch / cb["value"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[1]: Llama-3.1-8B attention shape, batch 16, 128K ctx, top-k 2048, "
-                               "head-wise cache + prefetch", "batch": args.batch, "ctx": args.ctx,
+        "config": {"workload": args.cfg["name"], "batch": args.batch, "ctx": args.ctx,
                    "layers": args.layers},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -222,8 +263,15 @@ def run_ours(args):
     from paper_2511_14510_b200.workload import synthetic_profiles, Shape
 
     lib = _lib.load()
-    B, L, HQ, H, d, n, k = (args.batch, args.layers, CONFIG2["q_heads"], CONFIG2["kv_heads"],
-                            CONFIG2["head_dim"], args.ctx, CONFIG2["k"])
+    C2 = args.cfg
+    B, L, HQ_all, H_all, d, n, k = (args.batch, args.layers, C2["q_heads"], C2["kv_heads"],
+                                    C2["head_dim"], args.ctx, C2["k"])
+    # KV-head sharding (configs[3]): this rank serves a contiguous block of KV
+    # heads for every sequence; request sharding: all heads of its own sequences.
+    shard_heads = C2["shard"] == "heads" and world > 1
+    from paper_2511_14510_b200.dist import kv_head_shard
+    hs = kv_head_shard(HQ_all, H_all, world if shard_heads else 1, rank if shard_heads else 0)
+    HQ, H = hs.n_q, hs.n_kv
     W, K = args.warmup, args.steps
     P = 2                       # profiled (instrumented-graph) steps
     E = 0 if args.no_e2e else K  # end-to-end (host buffers) steps
@@ -261,7 +309,29 @@ def run_ours(args):
         v = C.c_double()
         _lib.check(lib.clo_compute_threshold(s, eta, p, C.byref(v)))
         return v.value
-    tau, qimp = synthetic_profiles(Shape(L, HQ, H, d), seed=args.seed, threshold=thr)
+    tau, qimp = synthetic_profiles(Shape(L, HQ_all, H_all, d), seed=args.seed, threshold=thr)
+    persistent = np.zeros((L, H_all), np.int32)
+    persistent[0] = 1  # layer0_only_plan (engine.cpp:548-555)
+    plan_info = "layer0_only_plan"
+    if C2["plan"] == "partition":
+        # plan_partition (head_profile.cpp:80-154) over synthetic profiles:
+        # difficulty = tau - (s_hat - eps), eps = 0.05 (compute_difficulty :27-30),
+        # s_hat ~ U(0.5, 1) per head; N_p from a 50 us compute window at the
+        # measured-order PCIe bandwidth; HBM budget 80 GiB for the persistent KV
+        # of all `B` sequences.
+        rs = np.random.default_rng(args.seed + 17)
+        s_hat = rs.uniform(0.5, 1.0, (L, H_all))
+        diff = tau - (s_hat - 0.05)
+        pers = np.zeros((L, H_all), np.int32)
+        n_p, nd = C.c_int(), C.c_int()
+        row = 2 * d * 2
+        _lib.check(lib.clo_plan_partition(np.ascontiguousarray(diff).ctypes.data, L, H_all, 5e-5, 5.0e10,
+                                          float(2 * k * d * 2), row * (n + 4096) * B, 80 * (1 << 30),
+                                          pers.ctypes.data, C.byref(n_p), C.byref(nd)))
+        persistent = pers
+        plan_info = f"plan_partition: N_p={n_p.value}, persistent heads={int(pers.sum())}/{L * H_all}, dropped={nd.value}"
+    sl = slice(hs.kv0, hs.kv0 + hs.n_kv)
+    tau, qimp, persistent = tau[:, sl].copy(), qimp[:, sl].copy(), persistent[:, sl].copy()
 
     class _Src:  # StepSource shape for DecodeEngine's constructor (prompt already in hkv)
         n_prompt, steps, alias_layers = n, S, True
@@ -269,8 +339,11 @@ def run_ours(args):
 
     cfg = EngineConfig(shape=ModelShape(L, HQ, H, d, 2), k=k, sink_tokens=4, recent_tokens=64,
                        retriever="sign_hash", hash_bits=256, retriever_seed=1, policy="similarity",
-                       mode=ModeFlags(), batch=B, kv_dtype="bf16", device=local)
-    eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), layer0_only_plan(cfg.shape), _Src, host_kv=hkv)
+                       mode=ModeFlags(always_miss=C2["always_miss"]), batch=B, kv_dtype="bf16",
+                       kv_head_offset=hs.kv0, device=local)
+    from paper_2511_14510_b200.engine import PartitionPlan
+    plan = PartitionPlan(layers=[[g for g in range(H) if persistent[l, g]] for l in range(L)])
+    eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), plan, _Src, host_kv=hkv)
     t_pre = time.time()
     _lib.check(lib.clo_prefill(eng.h, tq[0].data_ptr(), 0, None))
     prefill_s = time.time() - t_pre
@@ -284,10 +357,14 @@ def run_ours(args):
         return _lib.StepIO(tq[t].data_ptr(), aq[t].data_ptr(), nk[t - 1].data_ptr(), nv[t - 1].data_ptr(),
                            out.data_ptr(), 0)
 
+    gathered_out = torch.empty((world, B, L, HQ, d), device=dev) if shard_heads else None
+
     def step_dev():
         t_idx[0] += 1
         io = dev_io(t_idx[0])
         _lib.check(lib.clo_decode_step(eng.h, C.byref(io), C.c_void_p(sp)))
+        if shard_heads:  # the path's one exchange: head outputs -> every rank (NCCL over NVLink)
+            dist.all_gather_into_tensor(gathered_out, out)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -322,7 +399,7 @@ def run_ours(args):
     launches = eng.kernel_launches() - launches0
     m1 = eng.metrics()
     ms_per_step = ms / K
-    value = world * B * K / (ms / 1e3)
+    value = (1 if shard_heads else world) * B * K / (ms / 1e3)
     hits = m1["hits"] - m0["hits"]
     misses = m1["misses"] - m0["misses"]
     gathered = m1["gathered_bytes_device"] - m0["gathered_bytes_device"]
@@ -379,7 +456,8 @@ def run_ours(args):
         ems = max_over_ranks(e0.elapsed_time(e1))
         h2d = (2 * B * L * HQ * d * 4) + 2 * B * L * H * d * 2
         d2h = B * L * HQ * d * 4
-        e2e = {"value": world * B * E / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": (1 if shard_heads else world) * B * E / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / E}
 
     # ---- PCIe link peak (pinned cudaMemcpy H2D, 1 GiB, best of 5) ----------
@@ -431,18 +509,19 @@ def run_ours(args):
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = reference_sample(args, steps=3, warmup=1, threads=args.cpu_threads or os.cpu_count() or 1)
+        cb = reference_sample(args, steps=3, warmup=1, threads=cpu_threads(args))
         cpu_baseline = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if shard_heads else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "configs[1]: Llama-3.1-8B attention shape (32 layers, 32q/8kv, d128), "
-                                   "batch 16 per GPU, 128K ctx, top-k 2048, head-wise cache + prefetch, "
-                                   "sign-hash 256b, layer 0 persistent",
-                       "batch_per_gpu": B, "ctx": n, "layers": L, "k": k, "parallelism": f"request-sharded x{world}",
+            "config": {"workload": C2["name"],
+                       "batch_per_gpu": B, "ctx": n, "layers": L, "k": k, "plan": plan_info,
+                       "parallelism": (f"kv-head-sharded x{world} (+NCCL all-gather)" if shard_heads
+                                       else f"request-sharded x{world}"),
                        "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
                        "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers",
                        "sigma_step": args.sigma, "sigma_layer": args.sigma_layer},

@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--n", type=int, default=131072)
     ap.add_argument("--rows", default="256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--huge", action="store_true", help="hugepage-backed pinned host store")
     args = ap.parse_args()
 
     import torch
@@ -51,7 +52,7 @@ def main():
     ptrs = []
     for _ in range(2):
         p = C.c_void_p()
-        _lib.check(lib.clo_host_alloc(nbytes, C.byref(p)))
+        _lib.check(lib.clo_host_alloc_ex(nbytes, _lib.HOST_HUGEPAGES if args.huge else 0, C.byref(p)))
         ptrs.append(p.value)
         arr = np.frombuffer((C.c_char * nbytes).from_address(p.value), dtype=np.uint16)
         arr[:] = np.random.default_rng(len(ptrs)).integers(0, 65535, arr.size, dtype=np.uint16)
@@ -79,7 +80,7 @@ def main():
         didx = torch.from_numpy(idx).to(dev)
         dst = torch.empty((2, H * r, d), dtype=torch.int16, device=dev)
         moved = 2 * H * r * row_bytes
-        line = {"rows_per_head": r, "heads": H, "bytes": moved}
+        line = {"rows_per_head": r, "heads": H, "bytes": moved, "n": n, "hugepages": args.huge}
         for name, engine in (("lsu", 0), ("tma", 1)):
             best = None
             for rep in range(args.reps + 1):

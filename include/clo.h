@@ -241,6 +241,12 @@ const char* clo_last_error(void);
 /* ------------------------------------------------------------------------ */
 /* Pinned host memory (UVA-mapped, portable): the host KV store.            */
 clo_status clo_host_alloc(size_t bytes, void** out);
+/* flags: CLO_HOST_HUGEPAGES backs the store with transparent huge pages
+ * (mmap + MADV_HUGEPAGE, then cudaHostRegister), so GPU threads reading random
+ * rows across a large store do not miss in the TLB on every 4 KiB page.
+ * Freed with clo_host_free. */
+#define CLO_HOST_HUGEPAGES 1
+clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out);
 clo_status clo_host_free(void* p);
 clo_status clo_host_register(void* p, size_t bytes);
 clo_status clo_host_unregister(void* p);

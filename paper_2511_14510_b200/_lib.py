@@ -22,6 +22,7 @@ RETRIEVER_EXACT, RETRIEVER_SIGN_HASH = 0, 1
 POLICY_SIMILARITY, POLICY_LRU, POLICY_LFU, POLICY_PREFETCH_ONLY = 0, 1, 2, 3
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
 SYNC_CPU_CENTRIC, SYNC_GPU_CENTRIC = 0, 1
+HOST_HUGEPAGES = 1
 
 
 class CloError(RuntimeError):
@@ -141,6 +142,7 @@ SIGNATURES = {
     "clo_nccl_get_unique_id": (_I, [_P]),
     "clo_last_error": (C.c_char_p, []),
     "clo_host_alloc": (_I, [C.c_size_t, C.POINTER(_P)]),
+    "clo_host_alloc_ex": (_I, [C.c_size_t, _I, C.POINTER(_P)]),
     "clo_host_free": (_I, [_P]),
     "clo_host_register": (_I, [_P, C.c_size_t]),
     "clo_host_unregister": (_I, [_P]),

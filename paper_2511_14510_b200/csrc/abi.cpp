@@ -1,7 +1,11 @@
 // abi.cpp — the C-ABI (include/clo.h): engine entry points, op-level entry
 // points and the host-side pure functions of the path.
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <numbers>
 #include <random>
@@ -210,14 +214,58 @@ clo_status clo_nccl_get_unique_id(void*) {
 
 // ----------------------------------------------------------------- host memory
 
-clo_status clo_host_alloc(size_t bytes, void** out) {
+namespace {
+// Hugepage-backed pinned allocations (mmap + MADV_HUGEPAGE + cudaHostRegister):
+// random 256-byte row reads spread over hundreds of MiB per head otherwise pay
+// GPU TLB misses on 4 KiB sysmem mappings.
+std::mutex g_huge_mu;
+std::unordered_map<void*, size_t> g_huge;
+}  // namespace
+
+clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out) {
     return guarded([&] {
         require_device();
-        CLO_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        if (!(flags & CLO_HOST_HUGEPAGES)) {
+            CLO_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+            return;
+        }
+        const size_t huge = size_t(2) << 20;
+        const size_t len = (bytes + huge - 1) / huge * huge;
+        void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) fail(CLO_ERR_IO, "mmap of the host K/V store failed");
+        madvise(p, len, MADV_HUGEPAGE);
+        std::memset(p, 0, len);  // fault the (huge) pages in before pinning
+        cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+        if (e != cudaSuccess) {
+            munmap(p, len);
+            cuda_check(e, "cudaHostRegister(hugepage store)");
+        }
+        std::lock_guard<std::mutex> lk(g_huge_mu);
+        g_huge[p] = len;
+        *out = p;
     });
 }
+
+clo_status clo_host_alloc(size_t bytes, void** out) { return clo_host_alloc_ex(bytes, 0, out); }
+
 clo_status clo_host_free(void* p) {
-    return guarded([&] { CLO_CUDA(cudaFreeHost(p)); });
+    return guarded([&] {
+        size_t len = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_huge_mu);
+            auto it = g_huge.find(p);
+            if (it != g_huge.end()) {
+                len = it->second;
+                g_huge.erase(it);
+            }
+        }
+        if (len) {
+            CLO_CUDA(cudaHostUnregister(p));
+            munmap(p, len);
+        } else {
+            CLO_CUDA(cudaFreeHost(p));
+        }
+    });
 }
 clo_status clo_host_register(void* p, size_t bytes) {
     return guarded([&] {

@@ -120,11 +120,13 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
     }
 }
 
-__global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L) {
+__global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L, int* claim, int* done) {
     if (threadIdx.x == 0) *dev_step += 1;
     for (int i = threadIdx.x; i < L; i += blockDim.x) {
         ca[i] = 0;
         cb[i] = 0;
+        if (claim) claim[i] = 0;
+        if (done) done[i] = 0;
     }
 }
 
@@ -194,7 +196,7 @@ void launch_append(const EngineView& v, int layer, cudaStream_t stream) {
 }
 
 void launch_step_end(const EngineView& v, int* count_a, int* count_b, cudaStream_t stream) {
-    step_end_kernel<<<1, 128, 0, stream>>>(v.dev_step, count_a, count_b, v.L);
+    step_end_kernel<<<1, 128, 0, stream>>>(v.dev_step, count_a, count_b, v.L, v.xfer_claim, v.xfer_done);
 }
 
 void launch_check_finite(const void* p, int dtype, int64_t count, int* err, int bit,

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <sstream>
+#include <string>
 #include <vector>
 
 #include "attention.cuh"
@@ -22,7 +23,30 @@ namespace clo {
 
 namespace {
 
-constexpr int64_t kGatherCtas = 48;
+// Gather CTAs: enough outstanding PCIe reads to cover the host round trip
+// without flooding the SMs the concurrent kernels need (CLO_GATHER_CTAS
+// overrides for experiments).
+int64_t gather_ctas() {
+    static const int64_t n = [] {
+        const char* e = getenv("CLO_GATHER_CTAS");
+        return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)48;
+    }();
+    return n;
+}
+
+// Transfer synchronisation. "events" (default): one gather launch per layer
+// on the transfer stream, ordered by graph edges (device-side dependencies,
+// no host sync). "flags" (CLO_TRANSFER=flags): one persistent transfer kernel
+// per step gated by device flags. The flag variant spins on flags set by
+// later launches, so tools that serialise kernels (ncu, compute-sanitizer)
+// would deadlock it; it is opt-in.
+bool use_flag_transfer() {
+    static const bool flags = [] {
+        const char* e = getenv("CLO_TRANSFER");
+        return e && std::string(e) == "flags";
+    }();
+    return flags;
+}
 
 int grid_for(int64_t units) {
     const int64_t cap = (int64_t)kNumSMs * 8;
@@ -197,6 +221,16 @@ void Engine::allocate() {
     max_attn_chunks_ = attention_chunks(k, cfg_.sink_tokens, cfg_.recent_tokens);
     d_attn_part_.alloc(sizeof(float) * B * H * max_attn_chunks_ * m * (d + 2), false);
     d_attn_count_.alloc(sizeof(int) * B * H);
+    d_xfer_.alloc(sizeof(int) * 5 * L);  // ready, units, claim, done, flag
+    {
+        std::vector<int> off;
+        for (int l = 0; l < L; ++l)
+            if (layer_has_off_[l]) off.push_back(l);
+        n_off_layers_ = (int)off.size();
+        d_off_layers_.alloc(sizeof(int) * std::max<size_t>(off.size(), 1));
+        if (!off.empty())
+            CLO_CUDA(cudaMemcpy(d_off_layers_.p, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+    }
 
     // staging for host-resident step inputs / outputs
     d_in_tq_.alloc(sizeof(float) * B * L * HQ * d, false);
@@ -341,6 +375,15 @@ EngineView Engine::view() const {
     v.attn_part = d_attn_part_.as<float>();
     v.attn_count = d_attn_count_.as<int>();
     v.max_attn_chunks = max_attn_chunks_;
+    {
+        int* x = d_xfer_.as<int>();
+        const int L = s.num_layers;
+        v.xfer_ready = x;
+        v.xfer_units = x + L;
+        v.xfer_claim = x + 2 * L;
+        v.xfer_done = x + 3 * L;
+        v.xfer_flag = x + 4 * L;
+    }
     return v;
 }
 
@@ -439,27 +482,31 @@ void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
     launches_ += 1;
 }
 
-void Engine::enqueue_gather(int layer, int count_bytes, cudaStream_t st) {
+GatherEngineArgs Engine::gather_args(int layer, int count_bytes) const {
     const SelScratch& sc = scratch_[1];
-    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
     GatherEngineArgs ga{};
     ga.v = view();
-    ga.items = sc.items + (size_t)layer * items;
+    ga.items = sc.items;  // base of the per-layer work lists
     ga.count = sc.count;
     ga.fetch_tok = sc.fetch_tok;
     ga.fetch_slot = sc.fetch_slot;
     ga.fetch_count = sc.fetch_count;
-    ga.items_cap = (int)items;
+    ga.items_cap = cfg_.batch * cfg_.shape.num_kv_heads;
     ga.layer = layer;
     ga.count_bytes = count_bytes;
+    return ga;
+}
+
+void Engine::enqueue_gather(int layer, int count_bytes, cudaStream_t st) {
+    const GatherEngineArgs ga = gather_args(layer, count_bytes);
     const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
     const int64_t vecs = (int64_t)cfg_.k * cfg_.shape.head_dim * esz / 16;
-    const int64_t units = (int64_t)items * ((vecs + 1023) / 1024);
+    const int64_t units = (int64_t)ga.items_cap * 2 * ((vecs + 2047) / 2048);
     prof_begin(st);
     // PCIe needs ~100 KB in flight (55 GB/s x ~2 us); each CTA keeps 32 KiB
     // outstanding, so a few dozen CTAs saturate the link and leave the SMs to
     // the selection and attention kernels running concurrently.
-    launch_gather_engine(ga, (int)std::min<int64_t>(units, kGatherCtas), st);
+    launch_gather_engine(ga, (int)std::min<int64_t>(units, gather_ctas()), st);
     prof_end(st, "gather_zero_copy", layer);
     launches_ += 1;
 }
@@ -623,6 +670,13 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
     if (!profiled) {
         CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_fork_, 0));
         CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_fork_, 0));
+        // one persistent transfer kernel per step streams every offloaded
+        // layer's fetch list as soon as the selection stream publishes it
+        if (n_off_layers_ > 0 && use_flag_transfer()) {
+            launch_gather_persistent(gather_args(0, 1), d_off_layers_.as<int>(), n_off_layers_,
+                                     (int)gather_ctas(), s_xfer);
+            launches_ += 1;
+        }
     }
     for (int l = 0; l < L; ++l) {
         if (layer_has_off_[l]) {
@@ -634,19 +688,32 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
             enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
             enqueue_select(1, l, s_pref);
             enqueue_reconcile(l, 0, s_pref);
-            CLO_CUDA(cudaEventRecord(ev_sel_[l], s_pref));
-            CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_sel_[l], 0));
-            enqueue_gather(l, 1, s_xfer);
-            CLO_CUDA(cudaEventRecord(ev_pref_[l], s_xfer));
+            if (profiled || !use_flag_transfer()) {
+                // one gather launch per layer, ordered by graph edges
+                CLO_CUDA(cudaEventRecord(ev_sel_[l], s_pref));
+                CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_sel_[l], 0));
+                enqueue_gather(l, 1, s_xfer);
+                CLO_CUDA(cudaEventRecord(ev_pref_[l], s_xfer));
+            } else {
+                launch_publish(gather_args(l, 1), s_pref);  // device flag for the transfer kernel
+                launches_ += 1;
+            }
         }
         if (layer_has_pers_[l]) {
             enqueue_prepare(0, l, kPrepDecode, kKindPersistent, s_main_);
             enqueue_select(0, l, s_main_);
         }
-        if (layer_has_off_[l]) CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_pref_[l], 0));
         prof_begin(s_main_);
         launch_append(view(), l, s_main_);
         prof_end(s_main_, "append", l);
+        if (layer_has_off_[l]) {  // layer l's rows must be in HBM before its attention
+            if (!profiled && use_flag_transfer()) {
+                launch_wait_flag(d_xfer_.as<int>() + 4 * cfg_.shape.num_layers + l, d_step_.as<int>(), s_main_);
+                launches_ += 1;
+            } else {
+                CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_pref_[l], 0));
+            }
+        }
         prof_begin(s_main_);
         if (!launch_attention_tma(view(), l, s_main_)) launch_attention_engine(view(), l, s_main_);
         prof_end(s_main_, "attention", l);
@@ -675,7 +742,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         CLO_CUDA(cudaGraphNodeGetType(nd, &t));
         kn += t == cudaGraphNodeTypeKernel;
     }
-    kernels_per_step_ = kn;
+    if (!profiled) kernels_per_step_ = kn;  // the production graph's kernel count
 }
 
 StepDesc Engine::make_desc(const clo_step_io& io, cudaStream_t user) {

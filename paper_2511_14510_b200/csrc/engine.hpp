@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "engine_view.h"
 #include "host_common.hpp"
+#include "gather.cuh"
 #include "select.cuh"
 
 namespace clo {
@@ -50,6 +51,7 @@ class Engine {
     void enqueue_select(int which, int layer, cudaStream_t st);
     void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
     void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
+    GatherEngineArgs gather_args(int layer, int count_bytes) const;
     void capture_graph(bool profiled, cudaGraph_t* graph, cudaGraphExec_t* exec);
     void prof_begin(cudaStream_t st);
     void prof_end(cudaStream_t st, const char* name, int layer);
@@ -74,7 +76,8 @@ class Engine {
     DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;
     DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
     DevBuf d_hits_, d_misses_, d_cache_last_, d_entry_last_, d_last_hit_, d_history_, d_gathered_;
-    DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_;
+    DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_, d_xfer_, d_off_layers_;
+    int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
     std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
     std::array<std::array<DevBuf, 16>, 2> scratch_bufs_;

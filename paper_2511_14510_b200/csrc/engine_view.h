@@ -109,6 +109,13 @@ struct EngineView {
     float* attn_part;      // [B*H][max_attn_chunks][m][d + 2]
     int* attn_count;       // [B*H] arrival counters (self-resetting)
     int max_attn_chunks;
+    // persistent transfer kernel (GPU-centric sync): per-layer device flags,
+    // epoch = the decode step they refer to
+    int* xfer_ready;       // [L] epoch when layer l's fetch lists are published
+    int* xfer_units;       // [L] work units of layer l
+    int* xfer_claim;       // [L] next unit to claim (reset at step end)
+    int* xfer_done;        // [L] units finished (reset at step end)
+    int* xfer_flag;        // [L] epoch when every unit of layer l landed in HBM
 };
 
 }  // namespace clo

@@ -25,6 +25,8 @@ namespace {
 constexpr int kGatherThreads = 256;
 constexpr int kUnroll = 4;
 constexpr int kVecsPerUnit = kGatherThreads * kUnroll;  // 16-byte vectors per work unit
+constexpr int kUnitUnroll = 8;                          // engine gather: loads in flight per thread
+constexpr int kUnitVecs = kGatherThreads * kUnitUnroll;  // 32 KiB of one matrix per unit
 constexpr int kRecThreads = 1024;
 
 __device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
@@ -121,56 +123,125 @@ __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a)
     }
 }
 
-// Work units = (missed head, block of fetch-list vectors).
-__global__ void __launch_bounds__(kGatherThreads) gather_engine_kernel(GatherEngineArgs a) {
+// Work units = (missed head, matrix, block of fetch-list vectors). K and V are
+// separate units (all of a head's K rows, then its V rows) so a CTA's
+// outstanding reads stay within one host matrix region at a time.
+__device__ __forceinline__ int gather_units_per_item(const EngineView& v) {
+    const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
+    return 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
+}
+
+// One work unit of layer `layer` (all threads of the CTA).
+__device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer, int u) {
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
-    const int units_per_item = (v.k * vpr + kVecsPerUnit - 1) / kVecsPerUnit;
-    const int count = a.count[a.layer];
-    const int units = count * units_per_item;
+    const int parts = (v.k * vpr + kUnitVecs - 1) / kUnitVecs;  // per matrix
+    const int units_per_item = 2 * parts;
     const size_t esz = dtype_size(v.kv_dtype);
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int item = u / units_per_item, part = u % units_per_item;
-        const size_t li = (size_t)a.layer * a.items_cap + item;
-        const int nf = a.fetch_count[li];
-        const int v0 = part * kVecsPerUnit;
-        const int v1 = min(nf * vpr, v0 + kVecsPerUnit);
-        if (v0 >= v1) continue;
-        const int seg = a.items[item].seg;
-        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
-        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
-        const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-        const uint4* src_k = reinterpret_cast<const uint4*>((const char*)v.host_k + base * esz);
-        const uint4* src_v = reinterpret_cast<const uint4*>((const char*)v.host_v + base * esz);
-        uint4* dst_k = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.k * row_bytes);
-        uint4* dst_v = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.k * row_bytes);
-        const int32_t* ftok = a.fetch_tok + li * v.k;
-        const int32_t* fslot = a.fetch_slot + li * v.k;
-        uint4 rk[kUnroll], rv[kUnroll];
-        size_t dsto[kUnroll];
+    const int item = u / units_per_item, rem = u % units_per_item;
+    const int mat = rem / parts, part = rem % parts;  // mat 0 = K, 1 = V
+    const size_t li = (size_t)layer * a.items_cap + item;
+    const int nf = a.fetch_count[li];
+    const int v0 = part * kUnitVecs;
+    const int v1 = min(nf * vpr, v0 + kUnitVecs);
+    if (v0 >= v1) return;
+    const int seg = a.items[(size_t)layer * a.items_cap + item].seg;
+    const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+    const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+    const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+    const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
+    uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.k * row_bytes);
+    const int32_t* ftok = a.fetch_tok + li * v.k;
+    const int32_t* fslot = a.fetch_slot + li * v.k;
+    uint4 r[kUnitUnroll];
+    size_t dsto[kUnitUnroll];
 #pragma unroll
-        for (int uu = 0; uu < kUnroll; ++uu) {
-            const int e = v0 + uu * kGatherThreads + threadIdx.x;
-            if (e < v1) {
-                const int r = e / vpr, c = e - r * vpr;
-                const size_t so = (size_t)ftok[r] * vpr + c;
-                dsto[uu] = (size_t)fslot[r] * vpr + c;
-                rk[uu] = src_k[so];
-                rv[uu] = src_v[so];
-            }
+    for (int uu = 0; uu < kUnitUnroll; ++uu) {
+        const int e = v0 + uu * kGatherThreads + threadIdx.x;
+        if (e < v1) {
+            const int row = e / vpr, c = e - row * vpr;
+            dsto[uu] = (size_t)fslot[row] * vpr + c;
+            r[uu] = src[(size_t)ftok[row] * vpr + c];
         }
-#pragma unroll
-        for (int uu = 0; uu < kUnroll; ++uu) {
-            const int e = v0 + uu * kGatherThreads + threadIdx.x;
-            if (e < v1) {
-                dst_k[dsto[uu]] = rk[uu];
-                dst_v[dsto[uu]] = rv[uu];
-            }
-        }
-        if (a.count_bytes && threadIdx.x == 0)
-            atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull * 2ull);
     }
+#pragma unroll
+    for (int uu = 0; uu < kUnitUnroll; ++uu) {
+        const int e = v0 + uu * kGatherThreads + threadIdx.x;
+        if (e < v1) dst[dsto[uu]] = r[uu];
+    }
+    if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+}
+
+// One launch per layer (prefill, and the serialised profiling graph).
+__global__ void __launch_bounds__(kGatherThreads) gather_engine_kernel(GatherEngineArgs a) {
+    const int units = a.count[a.layer] * gather_units_per_item(a.v);
+    for (int u = blockIdx.x; u < units; u += gridDim.x) gather_unit(a, a.layer, u);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Publishes layer l's fetch lists to the persistent transfer kernel (one
+// thread, on the selection stream after reconcile): unit count, then the
+// ready flag (release); a layer with nothing to fetch is marked done at once.
+__global__ void publish_kernel(GatherEngineArgs a) {
+    const EngineView& v = a.v;
+    const int epoch = *v.dev_step + 1;
+    const int units = a.count[a.layer] * gather_units_per_item(v);
+    v.xfer_units[a.layer] = units;
+    __threadfence();
+    if (units == 0) st_release(&v.xfer_flag[a.layer], epoch);
+    st_release(&v.xfer_ready[a.layer], epoch);
+}
+
+// Persistent transfer kernel: one launch per decode step on the high-priority
+// transfer stream. Its CTAs walk the offloaded layers in order; for each they
+// wait (device flag, no host involvement) until the layer's fetch lists are
+// published, claim work units from a per-layer counter and stream them from
+// pinned host memory into the HBM slots. The CTA finishing the layer's last
+// unit raises its done flag. Back-to-back layers leave no launch gaps on the
+// PCIe link.
+__global__ void __launch_bounds__(kGatherThreads) gather_persistent_kernel(GatherEngineArgs a,
+                                                                           const int* layers, int n_layers) {
+    const EngineView& v = a.v;
+    const int epoch = *v.dev_step + 1;
+    __shared__ int s_u, s_units;
+    for (int li = 0; li < n_layers; ++li) {
+        const int l = layers[li];
+        if (threadIdx.x == 0) {
+            while (ld_acquire(&v.xfer_ready[l]) != epoch) __nanosleep(128);
+            s_units = *((volatile int*)&v.xfer_units[l]);
+        }
+        __syncthreads();
+        const int units = s_units;
+        for (;;) {
+            if (threadIdx.x == 0) s_u = atomicAdd(&v.xfer_claim[l], 1);
+            __syncthreads();
+            const int u = s_u;
+            __syncthreads();
+            if (u >= units) break;
+            gather_unit(a, l, u);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&v.xfer_done[l], 1) + 1 == units) st_release(&v.xfer_flag[l], epoch);
+            }
+        }
+    }
+}
+
+// Compute-stream gate before attention(l): one thread waits for the layer's
+// done flag, so the stream proceeds without any host synchronisation.
+__global__ void wait_flag_kernel(const int* flag, const int* dev_step) {
+    const int epoch = *dev_step + 1;
+    while (ld_acquire(flag) != epoch) __nanosleep(128);
 }
 
 __global__ void __launch_bounds__(kGatherThreads) gather_op_kernel(const uint4* src, uint4* dst,
@@ -305,6 +376,17 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream) {
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
+}
+
+void launch_publish(const GatherEngineArgs& a, cudaStream_t stream) { publish_kernel<<<1, 1, 0, stream>>>(a); }
+
+void launch_gather_persistent(const GatherEngineArgs& a, const int* layers, int n_layers, int grid,
+                              cudaStream_t stream) {
+    gather_persistent_kernel<<<grid, kGatherThreads, 0, stream>>>(a, layers, n_layers);
+}
+
+void launch_wait_flag(const int* flag, const int* dev_step, cudaStream_t stream) {
+    wait_flag_kernel<<<1, 1, 0, stream>>>(flag, dev_step);
 }
 
 void launch_gather_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
