@@ -174,7 +174,12 @@ void launch_encode(const EncodeSeg* segs_dev, int n_segs, int64_t n, int d, int 
                    int* err, cudaStream_t stream) {
     if (n <= 0 || n_segs <= 0) return;
     dim3 grid((unsigned)((n + kEncRows - 1) / kEncRows), (unsigned)n_segs);
-    const size_t sm = (size_t)kEncRows * d * sizeof(double);
+    const size_t sm = (size_t)kEncRows * d * sizeof(double);  // 64 KiB at d = 256: opt in
+    if (sm > 48 * 1024) {
+        cudaFuncSetAttribute(encode_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(encode_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(encode_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    }
     switch (dtype) {
         case kBF16:
             encode_kernel<__nv_bfloat16><<<grid, kEncThreads, sm, stream>>>(segs_dev, n, d, bits, err);

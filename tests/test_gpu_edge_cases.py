@@ -1,0 +1,84 @@
+"""Edge cases of the decode path, CUDA engine vs the CPU oracle (same harness
+as test_gpu_engine.py: bit-exact selections/decisions/rows, outputs within
+tolerance)."""
+import numpy as np
+import pytest
+
+from tests.engine_harness import gpu_engine, make_case, run_and_compare
+
+pytestmark = pytest.mark.gpu
+
+
+def test_k_equals_prompt_selects_everything(oracle):
+    case = make_case(n_prompt=48, k=48, steps=5, sink=2, recent=8)
+    g, o, _ = run_and_compare(case, oracle)
+    assert list(g.head(1, 0)["entry_indices"][:3]) == [0, 1, 2]
+
+
+def test_k_one(oracle):
+    run_and_compare(make_case(k=1, steps=6), oracle)
+
+
+@pytest.mark.parametrize("sink,recent", [(0, 0), (0, 16), (4, 0), (8, 200)])
+def test_window_shapes(oracle, sink, recent):
+    run_and_compare(make_case(sink=sink, recent=recent, n_prompt=120, steps=6, k=8), oracle)
+
+
+@pytest.mark.parametrize("bits", [8, 64, 128, 192, 512])
+def test_hash_widths(oracle, bits):
+    run_and_compare(make_case(hash_bits=bits, steps=6), oracle)
+
+
+def test_tie_heavy_integer_keys_exact(oracle):
+    # integer-valued keys and queries: exact dot products collide massively;
+    # the (score desc, index asc) order decides every selection
+    case = make_case(retriever="exact", steps=8, k=12, sigma_step=0.3)
+    wl = case["wl"]
+    for arr in (wl.prompt_k, wl.new_k):
+        arr[...] = np.round(arr * 1.5)
+    for arr in (wl.true_q, wl.approx_q):
+        arr[...] = np.round(arr * 3)
+    run_and_compare(case, oracle)
+
+
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (16, 2)])
+def test_group_sizes_mha_and_m8(oracle, hq, hkv):
+    run_and_compare(make_case(hq=hq, hkv=hkv, steps=6, d=16), oracle)
+
+
+@pytest.mark.parametrize("d,kv_dtype", [(64, "bf16"), (256, "bf16"), (128, "f32"), (64, "f32")])
+def test_tma_attention_shapes(oracle, d, kv_dtype):
+    case = make_case(d=d, kv_dtype=kv_dtype, n_prompt=300, k=40, steps=5, sink=4, recent=64, hq=8, hkv=2)
+    _, _, worst = run_and_compare(case, oracle)
+    assert worst < 1e-5
+
+
+def test_acceptance_criterion_4_scale(oracle):
+    # acceptance_main.cpp:142-206: L=4, 4q/2kv, d=32, n=512, 200 steps,
+    # always_miss, exact retriever -> worst rel-L2 <= 1e-5 against the oracle
+    case = make_case(L=4, hq=4, hkv=2, d=32, n_prompt=512, steps=200, k=52, batch=1, retriever="exact",
+                     always_miss=True, kv_dtype="f32", sink=4, recent=64)
+    _, _, worst = run_and_compare(case, oracle, check_rows=False)
+    assert worst <= 1e-5
+
+
+def test_non_finite_prompt_raises_at_prefill():
+    from paper_2511_14510_b200._lib import NumericError
+    case = make_case(steps=2, kv_dtype="f32")
+    case["wl"].prompt_v[0, 1, 0, 5, 3] = np.inf
+    g = gpu_engine(case)
+    with pytest.raises(NumericError):
+        g.prefill()
+
+
+def test_invalid_configs_raise():
+    from paper_2511_14510_b200._lib import ArgumentError, ConfigError
+    for kw, exc in ((dict(k=0), ArgumentError), (dict(k=97), ArgumentError),
+                    (dict(always_miss=True, always_hit=True), ConfigError)):
+        case = make_case(**kw)
+        with pytest.raises(exc):
+            gpu_engine(case)
+    case = make_case(policy="prefetch_only")
+    case["cfg"].policy = "lru"  # block caches are outside the path
+    with pytest.raises(ConfigError):
+        gpu_engine(case)
