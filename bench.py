@@ -77,6 +77,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--same-device", action="store_true",
+                    help="testing only: every rank on cuda:0 with a gloo group (multi-rank functional check)")
+    ap.add_argument("--allgather", default="fused", choices=["fused", "nccl"],
+                    help="KV-head sharding exchange: fused into the attention epilogue over peer "
+                         "memory (default), or an NCCL all_gather after each step (baseline)")
     args = ap.parse_args()
     args.cfg = dict(CONFIGS[args.config])
     args.batch = args.batch or args.cfg["batch"]
@@ -252,11 +257,16 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_env()
+    if args.same_device:  # functional multi-rank check on a 1-GPU box (not a bench number)
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:  # NCCL refuses two ranks on one device; gloo carries the host plumbing
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2511_14510_b200 import _lib
     from paper_2511_14510_b200.engine import (DecodeEngine, EngineConfig, HostKV, ModelShape, ModeFlags,
                                               layer0_only_plan, profiles_from_arrays)
@@ -303,7 +313,9 @@ def run_ours(args):
         aq[t] = norm(q + args.sigma_layer * torch.randn(q.shape, generator=gen, device=dev))
     nk = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(torch.bfloat16).expand(S, B, L, H, d).contiguous()
     nv = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(torch.bfloat16).expand(S, B, L, H, d).contiguous()
-    out = torch.empty((B, L, HQ, d), device=dev)
+    fused_x = shard_heads and args.allgather == "fused"
+    HQo = HQ * world if fused_x else HQ  # out's head extent
+    out = torch.empty((B, L, HQo, d), device=dev)
 
     def thr(s, eta, p):
         v = C.c_double()
@@ -344,6 +356,9 @@ def run_ours(args):
     from paper_2511_14510_b200.engine import PartitionPlan
     plan = PartitionPlan(layers=[[g for g in range(H) if persistent[l, g]] for l in range(L)])
     eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), plan, _Src, host_kv=hkv)
+    if fused_x:  # head outputs travel inside the attention epilogue (exchange.cuh)
+        from paper_2511_14510_b200.dist import attach_head_exchange
+        attach_head_exchange(eng, rank, world)
     t_pre = time.time()
     _lib.check(lib.clo_prefill(eng.h, tq[0].data_ptr(), 0, None))
     prefill_s = time.time() - t_pre
@@ -363,8 +378,8 @@ def run_ours(args):
         t_idx[0] += 1
         io = dev_io(t_idx[0])
         _lib.check(lib.clo_decode_step(eng.h, C.byref(io), C.c_void_p(sp)))
-        if shard_heads:  # the path's one exchange: head outputs -> every rank (NCCL over NVLink)
-            dist.all_gather_into_tensor(gathered_out, out)
+        if shard_heads and not fused_x:  # baseline exchange: NCCL all-gather after the step
+            dist.all_gather(list(gathered_out.unbind(0)), out)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -375,7 +390,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if dist is None:
             return x
-        tt = torch.tensor([x], device=dev, dtype=torch.float64)
+        tt = torch.tensor([x], device="cpu" if args.same_device else dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
@@ -432,7 +447,7 @@ def run_ours(args):
         h_aq = torch.empty_like(h_tq, pin_memory=True)
         h_nk = torch.empty((E + W, B, L, H, d), dtype=torch.bfloat16, pin_memory=True)
         h_nv = torch.empty_like(h_nk, pin_memory=True)
-        h_out = torch.empty((B, L, HQ, d), pin_memory=True)
+        h_out = torch.empty((B, L, HQo, d), pin_memory=True)
         base = t_idx[0]
         h_tq.copy_(tq[base + 1: base + 1 + E + W])
         h_aq.copy_(aq[base + 1: base + 1 + E + W])
@@ -455,7 +470,7 @@ def run_ours(args):
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
         h2d = (2 * B * L * HQ * d * 4) + 2 * B * L * H * d * 2
-        d2h = B * L * HQ * d * 4
+        d2h = B * L * HQo * d * 4
         e2e = {"value": (1 if shard_heads else world) * B * E / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / E}
@@ -520,7 +535,8 @@ def run_ours(args):
             "dtype": "bf16", "data": "synthetic",
             "config": {"workload": C2["name"],
                        "batch_per_gpu": B, "ctx": n, "layers": L, "k": k, "plan": plan_info,
-                       "parallelism": (f"kv-head-sharded x{world} (+NCCL all-gather)" if shard_heads
+                       "parallelism": (f"kv-head-sharded x{world} (+{'fused P2P' if fused_x else 'NCCL'} "
+                                       f"head-output all-gather)" if shard_heads
                                        else f"request-sharded x{world}"),
                        "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
                        "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers",

@@ -39,13 +39,15 @@ def main():
     ap.add_argument("--rows", default="256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--huge", action="store_true", help="hugepage-backed pinned host store")
+    ap.add_argument("--d", type=int, default=128, help="row width in bf16 elements (256 = K|V interleaved row)")
+    ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
 
     import torch
     from paper_2511_14510_b200 import _lib
     lib = _lib.load()
     dev = torch.device("cuda", 0)
-    d, esz, n, H = 128, 2, args.n, args.heads
+    d, esz, n, H = args.d, 2, args.n, args.heads
     row_bytes = d * esz
     # host store: H heads x n rows, K and V, pinned + mapped
     nbytes = H * n * row_bytes
@@ -103,6 +105,12 @@ def main():
             line[f"{name}_ms"] = best
             line[f"{name}_gbs"] = moved / (best * 1e-3) / 1e9
         # gather-copy baseline: CPU threads gather into pinned staging, then H2D
+        if args.skip_cpu:
+            line["link_peak_gbs"] = peak
+            line["lsu_frac_of_peak"] = line["lsu_gbs"] / peak
+            results.append(line)
+            print(json.dumps(line), flush=True)
+            continue
         stg = C.c_void_p()
         _lib.check(lib.clo_host_alloc(H * r * row_bytes, C.byref(stg)))
         hidx = np.ascontiguousarray(idx)
@@ -132,7 +140,8 @@ def main():
                       "link_peak_gbs_pinned_memcpy": peak, "pcie_gen5_x16_theoretical_gbs": 64.0,
                       "best_lsu_gbs": max(x["lsu_gbs"] for x in results),
                       "best_tma_gbs": max(x["tma_gbs"] for x in results),
-                      "best_cpu_staged_gbs": max(x["cpu_staged_gbs"] for x in results)}), flush=True)
+                      "best_cpu_staged_gbs": max((x.get("cpu_staged_gbs", 0.0) for x in results))}),
+          flush=True)
 
 
 if __name__ == "__main__":

@@ -228,13 +228,30 @@ uint64_t clo_engine_kernel_launches(const clo_engine* e);
 /* Kernels per decode step (graph nodes that are kernels). */
 int clo_engine_kernels_per_step(const clo_engine* e);
 
-/* Multi-GPU (KV-head sharding): attach an NCCL communicator
- * (ncclUniqueId bytes from rank 0, 128 bytes) so every layer's head outputs
- * [B][hq_local][d] are all-gathered into io->out laid out [B][L][hq_global][d]
- * inside the step graph. world == 1 detaches. */
-clo_status clo_engine_attach_nccl(clo_engine* e, const void* nccl_unique_id, int rank,
-                                  int world);
-clo_status clo_nccl_get_unique_id(void* out128);
+/* Multi-GPU (KV-head sharding): the head-output all-gather,
+ * fused into the attention epilogue over peer memory (no NCCL launch).
+ * The reference has no distributed path; this replaces the one exchange the
+ * sharded step needs: every layer's per-head outputs (engine.cpp:403-405,
+ * collected_outputs [t][l] -> h_q x d) reaching every rank.
+ *
+ * Rank r's engine serves KV heads [r*H, (r+1)*H) of a model with world*H KV
+ * heads (cfg.kv_head_offset = r*H; shape.num_*_heads are the LOCAL counts).
+ * Protocol (one process or thread per rank, any host transport for the
+ * handle bytes, e.g. torch.distributed.all_gather_object):
+ *   1. clo_engine_exchange_handle(e, rank, world, h)   -> CLO_EXCHANGE_HANDLE_BYTES
+ *   2. exchange the handles; handles[r] = rank r's bytes, concatenated
+ *   3. clo_engine_attach_peers(e, handles), then a host barrier
+ * From then on io->out of every step is [B][L][world*hq][d]: the attention
+ * kernels store each head's output into out and into every peer's exchange
+ * slot (P2P stores over NVLink, CUDA IPC mappings across processes), raise a
+ * per-layer arrival counter with a system-scope release, and the last kernel
+ * of the step graph acquires the counters and copies the peers' blocks.
+ * Ranks must step in lockstep; a peer that stops stepping surfaces as
+ * CLO_ERR_CUDA ("exchange timed out") at the next synchronising call.
+ * Must be called before the first decode step. */
+#define CLO_EXCHANGE_HANDLE_BYTES 256
+clo_status clo_engine_exchange_handle(clo_engine* e, int rank, int world, void* handle_out);
+clo_status clo_engine_attach_peers(clo_engine* e, const void* handles);
 
 const char* clo_last_error(void);
 

@@ -23,6 +23,7 @@ POLICY_SIMILARITY, POLICY_LRU, POLICY_LFU, POLICY_PREFETCH_ONLY = 0, 1, 2, 3
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
 SYNC_CPU_CENTRIC, SYNC_GPU_CENTRIC = 0, 1
 HOST_HUGEPAGES = 1
+EXCHANGE_HANDLE_BYTES = 256  # CLO_EXCHANGE_HANDLE_BYTES
 
 
 class CloError(RuntimeError):
@@ -138,8 +139,8 @@ SIGNATURES = {
     "clo_engine_profile_step": (_I, [_P, C.POINTER(StepIO), _P, C.POINTER(KernelTime), _I, C.POINTER(_I)]),
     "clo_engine_kernel_launches": (_U64, [_P]),
     "clo_engine_kernels_per_step": (_I, [_P]),
-    "clo_engine_attach_nccl": (_I, [_P, _P, _I, _I]),
-    "clo_nccl_get_unique_id": (_I, [_P]),
+    "clo_engine_exchange_handle": (_I, [_P, _I, _I, _P]),
+    "clo_engine_attach_peers": (_I, [_P, _P]),
     "clo_last_error": (C.c_char_p, []),
     "clo_host_alloc": (_I, [C.c_size_t, C.POINTER(_P)]),
     "clo_host_alloc_ex": (_I, [C.c_size_t, _I, C.POINTER(_P)]),

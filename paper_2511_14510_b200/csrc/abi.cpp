@@ -202,14 +202,18 @@ int clo_engine_kernels_per_step(const clo_engine* e) {
     return reinterpret_cast<const Engine*>(e)->kernels_per_step();
 }
 
-clo_status clo_engine_attach_nccl(clo_engine*, const void*, int, int world) {
+clo_status clo_engine_exchange_handle(clo_engine* e, int rank, int world, void* handle_out) {
     return guarded([&] {
-        if (world != 1) fail(CLO_ERR_CONFIG, "in-graph NCCL all-gather is not built in this library version");
+        if (!e || !handle_out) fail(CLO_ERR_ARGUMENT, "null argument");
+        reinterpret_cast<Engine*>(e)->peer_handle(rank, world, handle_out);
     });
 }
 
-clo_status clo_nccl_get_unique_id(void*) {
-    return guarded([&] { fail(CLO_ERR_CONFIG, "NCCL is not linked into this library version"); });
+clo_status clo_engine_attach_peers(clo_engine* e, const void* handles) {
+    return guarded([&] {
+        if (!e || !handles) fail(CLO_ERR_ARGUMENT, "null argument");
+        reinterpret_cast<Engine*>(e)->attach_peers(handles);
+    });
 }
 
 // ----------------------------------------------------------------- host memory

@@ -4,6 +4,7 @@
 #include <math_constants.h>
 
 #include "attention.cuh"
+#include "exchange.cuh"
 
 namespace clo {
 
@@ -251,7 +252,6 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    float* out = v.desc->out;
     for (int i = threadIdx.x; i < M * D; i += blockDim.x) {
         const int j = i / D, e = i % D;
         const float* pb = v.attn_part + (size_t)bg * v.max_attn_chunks * M * (D + 2) + j * (D + 2);
@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
             a += __ldcg(pb + cc * stride + e) * cw;
             s += __ldcg(pb + cc * stride + D + 1) * cw;
         }
-        if (out) out[(((size_t)b * v.L + l) * v.HQ + (size_t)g * M + j) * D + e] = a / s;
+        emit_head_output(v, t, b, l, g * M + j, e, a / s);
     }
+    signal_head_output(v, l);
     if (threadIdx.x == 0) v.attn_count[bg] = 0;
 }
 

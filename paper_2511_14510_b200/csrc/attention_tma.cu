@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "attention.cuh"
+#include "exchange.cuh"
 
 namespace clo {
 
@@ -481,7 +482,6 @@ __global__ void __launch_bounds__(kThreads, 4) attn_tma_kernel(EngineView v, int
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    float* out = v.desc->out;
     const float* pb = v.attn_part + (size_t)bg * v.max_attn_chunks * M * (D + 2);
     const size_t stride = (size_t)M * (D + 2);
     for (int i = threadIdx.x; i < M * D; i += blockDim.x) {
@@ -494,8 +494,9 @@ __global__ void __launch_bounds__(kThreads, 4) attn_tma_kernel(EngineView v, int
             a += __ldcg(pb + cc * stride + j * (D + 2) + e) * cw;
             s += __ldcg(pb + cc * stride + j * (D + 2) + D + 1) * cw;
         }
-        if (out) out[(((size_t)b * v.L + l) * v.HQ + (size_t)g * M + j) * D + e] = a / s;
+        emit_head_output(v, t, b, l, g * M + j, e, a / s);
     }
+    signal_head_output(v, l);
     if (threadIdx.x == 0) v.attn_count[bg] = 0;
 }
 

@@ -13,6 +13,7 @@ constexpr int kMaxGroup = 16;      // m = hq / hkv
 constexpr int kMaxHeadDim = 256;
 constexpr int kScoreChunk = 4096;  // rows per score/compact work unit
 constexpr int kScoreThreads = 256;
+constexpr int kMaxRanks = 8;      // KV-head shards of one model (one NVSwitch node)
 
 enum DType : int { kBF16 = 0, kF32 = 1, kF64 = 2 };
 
@@ -66,6 +67,7 @@ enum ErrBits : int {
     kErrDuplicate = 16,
     kErrContract = 32,
     kErrInternal = 64,
+    kErrExchange = 128,  // head-output exchange: a peer stopped arriving
 };
 
 __device__ __forceinline__ void raise_err(int* flag, int bits) {

@@ -9,12 +9,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <unistd.h>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "attention.cuh"
 #include "encode.cuh"
+#include "exchange.cuh"
 #include "gather.cuh"
 #include "lookup.cuh"
 #include "select.cuh"
@@ -46,6 +48,17 @@ bool use_flag_transfer() {
         return e && std::string(e) == "flags";
     }();
     return flags;
+}
+
+// A peer whose arrivals are missing this long has stopped stepping (not a
+// slow one); CLO_EXCHANGE_TIMEOUT_MS overrides the 20 s default.
+unsigned long long exchange_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* e = getenv("CLO_EXCHANGE_TIMEOUT_MS");
+        const long long ms = e ? atoll(e) : 0;
+        return (unsigned long long)(ms > 0 ? ms : 20000) * 1000000ull;
+    }();
+    return ns;
 }
 
 int grid_for(int64_t units) {
@@ -129,6 +142,8 @@ Engine::Engine(const clo_engine_config& cfg, const double* tau, const double* q_
 
 Engine::~Engine() {
     cudaSetDevice(cfg_.device);
+    for (int r = 0; r < kMaxRanks; ++r)
+        if (xipc_[r]) cudaIpcCloseMemHandle(xbase_[r]);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (graph_) cudaGraphDestroy(graph_);
     if (pgraph_exec_) cudaGraphExecDestroy(pgraph_exec_);
@@ -384,6 +399,16 @@ EngineView Engine::view() const {
         v.xfer_done = x + 3 * L;
         v.xfer_flag = x + 4 * L;
     }
+    v.world = world_;
+    v.rank = rank_;
+    v.xtimeout_ns = exchange_timeout_ns();
+    v.HQg = world_ * s.num_q_heads;
+    v.q0 = rank_ * s.num_q_heads;
+    for (int r = 0; r < world_; ++r) {
+        char* base = static_cast<char*>(xbase_[r]);
+        v.xflag[r] = reinterpret_cast<unsigned*>(base);
+        v.xslot[r] = reinterpret_cast<float*>(base + exchange_flag_bytes(s.num_layers));
+    }
     return v;
 }
 
@@ -538,6 +563,108 @@ void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_st
         cudaGraphDestroy(pgraph_);
         pgraph_exec_ = nullptr;
         pgraph_ = nullptr;
+    }
+}
+
+namespace {
+// Exchange handle: what a peer needs to map this engine's exchange buffer.
+// Engines in the same process (same pid) share the pointer directly; other
+// processes open the CUDA IPC handle (peer access over NVLink when the
+// devices differ, a plain mapping when they share one).
+struct ExchangeHandle {
+    uint32_t magic;
+    int32_t pid, device, rank, world, B, L, HQg, d;
+    uint64_t base, bytes;
+    cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kExchangeMagic = 0xC10E8C01u;
+static_assert(sizeof(ExchangeHandle) <= CLO_EXCHANGE_HANDLE_BYTES, "exchange handle too large");
+}  // namespace
+
+void Engine::peer_handle(int rank, int world, void* out) {
+    const clo_model_shape& s = cfg_.shape;
+    if (world < 1 || world > kMaxRanks) fail(CLO_ERR_CONFIG, "world must be in [1, 8]");
+    if (rank < 0 || rank >= world) fail(CLO_ERR_ARGUMENT, "rank out of range");
+    if (cfg_.kv_head_offset != rank * s.num_kv_heads)
+        fail(CLO_ERR_CONFIG, "KV-head shards must be contiguous blocks: kv_head_offset != rank * num_kv_heads");
+    if (steps_ > 0) fail(CLO_ERR_CONTRACT, "attach the exchange before the first decode step");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    const int HQg = world * s.num_q_heads;
+    const size_t bytes = exchange_flag_bytes(s.num_layers) +
+                         sizeof(float) * 2 * (size_t)cfg_.batch * s.num_layers * HQg * s.head_dim;
+    d_xbuf_.alloc(bytes);  // zeroed: counters start at 0
+    d_out_.alloc(sizeof(float) * (size_t)cfg_.batch * s.num_layers * HQg * s.head_dim, false);
+    world_ = 1;  // until attach_peers succeeds
+    rank_ = rank;
+    ExchangeHandle h{};
+    h.magic = kExchangeMagic;
+    h.pid = (int32_t)getpid();
+    h.device = cfg_.device;
+    h.rank = rank;
+    h.world = world;
+    h.B = cfg_.batch;
+    h.L = s.num_layers;
+    h.HQg = HQg;
+    h.d = s.head_dim;
+    h.base = (uint64_t)(uintptr_t)d_xbuf_.p;
+    h.bytes = bytes;
+    CLO_CUDA(cudaIpcGetMemHandle(&h.ipc, d_xbuf_.p));
+    std::memset(out, 0, CLO_EXCHANGE_HANDLE_BYTES);
+    std::memcpy(out, &h, sizeof h);
+}
+
+void Engine::attach_peers(const void* handles) {
+    if (!d_xbuf_.p) fail(CLO_ERR_CONTRACT, "export this engine's exchange handle first");
+    if (steps_ > 0) fail(CLO_ERR_CONTRACT, "attach the exchange before the first decode step");
+    CLO_CUDA(cudaSetDevice(cfg_.device));
+    ExchangeHandle self{};
+    std::memcpy(&self, static_cast<const char*>(handles) + (size_t)rank_ * CLO_EXCHANGE_HANDLE_BYTES, sizeof self);
+    if (self.magic != kExchangeMagic || self.base != (uint64_t)(uintptr_t)d_xbuf_.p)
+        fail(CLO_ERR_ARGUMENT, "handles[rank] is not this engine's exchange handle");
+    const int world = self.world;
+    for (int r = 0; r < kMaxRanks; ++r)
+        if (xipc_[r]) {
+            cudaIpcCloseMemHandle(xbase_[r]);
+            xipc_[r] = false;
+        }
+    xbase_.fill(nullptr);
+    for (int r = 0; r < world; ++r) {
+        ExchangeHandle h{};
+        std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * CLO_EXCHANGE_HANDLE_BYTES, sizeof h);
+        if (h.magic != kExchangeMagic) fail(CLO_ERR_ARGUMENT, "malformed exchange handle");
+        if (h.rank != r || h.world != world || h.B != self.B || h.L != self.L || h.HQg != self.HQg || h.d != self.d)
+            fail(CLO_ERR_CONFIG, "exchange handles disagree on rank order, world or output shape");
+        if (r == rank_) {
+            xbase_[r] = d_xbuf_.p;
+        } else if (h.pid == self.pid) {  // same process: the pointer is valid here
+            if (h.device != cfg_.device) {
+                int ok = 0;
+                CLO_CUDA(cudaDeviceCanAccessPeer(&ok, cfg_.device, h.device));
+                if (!ok) fail(CLO_ERR_CUDA, "no peer access between the shards' devices");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CLO_CUDA(e);
+                cudaGetLastError();
+            }
+            xbase_[r] = (void*)(uintptr_t)h.base;
+        } else {
+            void* p = nullptr;
+            CLO_CUDA(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+            xbase_[r] = p;
+            xipc_[r] = true;
+        }
+    }
+    world_ = world;
+    for (auto* g : {&graph_, &pgraph_}) {  // views are baked into the graphs
+        if (*g) {
+            cudaGraphDestroy(*g);
+            *g = nullptr;
+        }
+    }
+    for (auto* x : {&graph_exec_, &pgraph_exec_}) {
+        if (*x) {
+            cudaGraphExecDestroy(*x);
+            *x = nullptr;
+        }
     }
 }
 
@@ -726,6 +853,12 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         CLO_CUDA(cudaEventRecord(ev_join2_, s_xfer));
         CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join2_, 0));
     }
+    if (world_ > 1) {  // peers' head outputs of this step -> out (exchange.cuh)
+        prof_begin(s_main_);
+        launch_exchange_finish(view(), s_main_);
+        prof_end(s_main_, "exchange_finish", -1);
+        launches_ += 1;
+    }
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
     CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
@@ -781,7 +914,7 @@ std::vector<clo_kernel_time> Engine::profile_step(const clo_step_io& io, cudaStr
     CLO_CUDA(cudaGraphLaunch(pgraph_exec_, user));
     launches_ += kernels_per_step_;
     if (io.on_host && io.out)
-        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * cfg_.batch * s.num_layers * s.num_q_heads * s.head_dim,
+        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * cfg_.batch * s.num_layers * world_ * s.num_q_heads * s.head_dim,
                                  cudaMemcpyDeviceToHost, user));
     ++steps_;
     CLO_CUDA(cudaStreamSynchronize(user));
@@ -810,7 +943,8 @@ void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
     CLO_CUDA(cudaGraphLaunch(graph_exec_, user));
     launches_ += kernels_per_step_;
     if (io.on_host && io.out)
-        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * B * L * HQ * d, cudaMemcpyDeviceToHost, user));
+        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * B * L * world_ * HQ * d, cudaMemcpyDeviceToHost,
+                                 user));
     CLO_CUDA(cudaGetLastError());
     ++steps_;
 }
@@ -830,6 +964,8 @@ void Engine::check_device_error() {
     if (err & kErrNonFiniteKey) fail(CLO_ERR_NUMERIC, "non-finite key entry");
     if (err & kErrNonFiniteValue) fail(CLO_ERR_NUMERIC, "non-finite value entry");
     if (err & kErrContract) fail(CLO_ERR_CONTRACT, "device-side contract violation");
+    if (err & kErrExchange)
+        fail(CLO_ERR_CUDA, "head-output exchange timed out: a peer rank stopped stepping");
     fail(CLO_ERR_INTERNAL, "device-side error flag " + std::to_string(err));
 }
 

@@ -37,6 +37,12 @@ class Engine {
     // measured inside the graph (bench roofline). Synchronous.
     std::vector<clo_kernel_time> profile_step(const clo_step_io& io, cudaStream_t user);
 
+    // KV-head sharding: fused head-output all-gather over peer memory
+    // (exchange.cuh). peer_handle() describes this engine's exchange buffer;
+    // attach_peers() maps every rank's buffer (P2P / CUDA IPC).
+    void peer_handle(int rank, int world, void* out);
+    void attach_peers(const void* handles);
+
     uint64_t launches() const { return launches_; }
     int kernels_per_step() const { return kernels_per_step_; }
     const clo_engine_config& config() const { return cfg_; }
@@ -102,6 +108,12 @@ class Engine {
     std::vector<cudaEvent_t> desc_ev_;
     std::vector<int> desc_used_;
     int desc_next_ = 0;
+
+    // head-output exchange
+    int world_ = 1, rank_ = 0;
+    DevBuf d_xbuf_;                        // [flags][2][B][L][HQg][d]
+    std::array<void*, kMaxRanks> xbase_{};  // every rank's exchange buffer, mapped here
+    std::array<bool, kMaxRanks> xipc_{};    // opened through cudaIpcOpenMemHandle
 
     bool prefilled_ = false;
     int steps_ = 0;

@@ -25,6 +25,8 @@
 
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace clo {
 
 struct SelItem;
@@ -116,6 +118,14 @@ struct EngineView {
     int* xfer_claim;       // [L] next unit to claim (reset at step end)
     int* xfer_done;        // [L] units finished (reset at step end)
     int* xfer_flag;        // [L] epoch when every unit of layer l landed in HBM
+    // head-output exchange (KV-head sharding, exchange.cuh). world == 1: none;
+    // out is then [B][L][HQ][d] (HQg == HQ, q0 == 0).
+    int world, rank;
+    int HQg;               // query heads of the whole model (out's head extent)
+    int q0;                // first global query head of this shard
+    float* xslot[kMaxRanks];     // rank r's exchange slots [2][B][L][HQg][d]
+    unsigned* xflag[kMaxRanks];  // rank r's per-layer arrival counters [L]
+    unsigned long long xtimeout_ns;  // a peer silent this long is reported lost
 };
 
 }  // namespace clo

@@ -55,6 +55,25 @@ def allgather_heads(local, group=None):
     return torch.cat(parts, dim=2)
 
 
+def attach_head_exchange(engine, rank: int, world: int, group=None) -> None:
+    """Fused head-output all-gather (include/clo.h, exchange.cuh): every rank
+    exports its engine's exchange handle, the handles travel over the host
+    process group (torch.distributed plumbing: gloo or NCCL object
+    all-gather), each engine maps its peers' buffers, then a barrier so no
+    rank steps before every peer is attached. After this the attention
+    epilogues store head outputs straight into the peers' memory; there is no
+    per-step collective launch."""
+    import torch.distributed as dist
+    mine = engine.exchange_handle(rank, world)
+    if world == 1:
+        engine.attach_peers([mine])
+        return
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    engine.attach_peers(handles)
+    dist.barrier(group=group)
+
+
 def max_over_ranks(x: float, device=None, group=None) -> float:
     """Device time of a multi-rank region = the slowest rank's."""
     import torch

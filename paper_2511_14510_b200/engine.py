@@ -208,6 +208,7 @@ class DecodeEngine:
                                                ss, 0 if Lk == 1 else ls, hs))
         self.current_step = 0
         self._outputs = []
+        self.world = 1
 
     def close(self):
         if getattr(self, "h", None):
@@ -230,7 +231,7 @@ class DecodeEngine:
         aq = np.ascontiguousarray(self.source.approx_q[t], np.float32)
         nk, nv = self.source.step_new_kv(t)
         s = self.cfg.shape
-        out = np.empty((self.cfg.batch, s.num_layers, s.num_q_heads, s.head_dim), np.float32)
+        out = np.empty((self.cfg.batch, s.num_layers, self.world * s.num_q_heads, s.head_dim), np.float32)
         io = _lib.StepIO(ptr(tq), ptr(aq), ptr(nk), ptr(nv), ptr(out), 1)
         check(self.lib.clo_decode_step(self.h, C.byref(io), None))
         check(self.lib.clo_engine_synchronize(self.h))
@@ -284,6 +285,21 @@ class DecodeEngine:
 
     def cache_state(self, seq: int = 0) -> dict:
         return json.loads(self.cache_state_json(seq))
+
+    # -- KV-head sharding: fused head-output exchange (include/clo.h) ---------
+    def exchange_handle(self, rank: int, world: int) -> bytes:
+        """This engine's exchange handle (step 1 of the attach protocol)."""
+        buf = (C.c_char * _lib.EXCHANGE_HANDLE_BYTES)()
+        check(self.lib.clo_engine_exchange_handle(self.h, rank, world, buf))
+        self._pending_world = world
+        return bytes(buf)
+
+    def attach_peers(self, handles) -> None:
+        """Maps every rank's exchange buffer (handles in rank order); from the
+        next step on, outputs cover the whole model's query heads."""
+        blob = b"".join(handles)
+        check(self.lib.clo_engine_attach_peers(self.h, blob))
+        self.world = getattr(self, "_pending_world", len(handles))
 
     def kernel_launches(self) -> int:
         return self.lib.clo_engine_kernel_launches(self.h)

@@ -108,3 +108,47 @@ def test_shard_plans():
     assert (sh.kv0, sh.n_kv, sh.q0, sh.n_q) == (4, 2, 16, 8)
     with pytest.raises(ValueError):
         kv_head_shard(32, 8, 3, 0)
+
+
+class _FakeEngine:
+    """Stands in for DecodeEngine in the host half of the exchange protocol."""
+
+    def __init__(self, rank):
+        self.rank, self.attached = rank, None
+
+    def exchange_handle(self, rank, world):
+        assert rank == self.rank
+        return bytes([rank]) * 256
+
+    def attach_peers(self, handles):
+        self.attached = list(handles)
+
+
+def _exchange_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_14510_b200.dist import attach_head_exchange
+        e = _FakeEngine(rank)
+        attach_head_exchange(e, rank, world)
+        q.put((rank, e.attached))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_exchange_handles_travel_in_rank_order():
+    """Host plumbing of the fused head-output all-gather (dist.attach_head_exchange):
+    every rank ends up with all handles, in rank order, before anyone steps."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert got[r] == [bytes([0]) * 256, bytes([1]) * 256]
