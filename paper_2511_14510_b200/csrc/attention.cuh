@@ -23,6 +23,12 @@ int attention_chunks(int k, int sink, int recent);
 bool attention_tma_supported(int dtype, int d, int m, int k);
 bool launch_attention_tma(const EngineView& v, int layer, cudaStream_t stream);
 bool attention_supported(int dtype, int d, int m);
+// Tensor-core production kernel (attention_mma.cu): bf16 rows, d 64/128,
+// m <= 8; false = unsupported (or CLO_ATTN=tma|ffma), try the TMA kernel.
+bool attention_mma_supported(int dtype, int d, int m, int k);
+bool launch_attention_mma(const EngineView& v, int layer, cudaStream_t stream);
+// floats of attn_part the tensor-core kernel's per-warp partials need
+size_t attention_mma_partial_floats(int B, int H, int m, int d, int k, int sink, int recent);
 
 // Op-level topk_attention for m queries over one matrix (validation separate).
 void launch_attention_op(const double* q, int m, const void* keys, const void* values, int dtype,

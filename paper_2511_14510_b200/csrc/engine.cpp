@@ -234,8 +234,11 @@ void Engine::allocate() {
     d_desc_.alloc(sizeof(StepDesc));
     d_err_.alloc(sizeof(int));
     max_attn_chunks_ = attention_chunks(k, cfg_.sink_tokens, cfg_.recent_tokens);
-    d_attn_part_.alloc(sizeof(float) * B * H * max_attn_chunks_ * m * (d + 2), false);
-    d_attn_count_.alloc(sizeof(int) * B * H);
+    d_attn_part_.alloc(sizeof(float) * std::max<size_t>((size_t)B * H * max_attn_chunks_ * m * (d + 2),
+                                                         attention_mma_partial_floats(B, H, m, d, k, cfg_.sink_tokens,
+                                                                                      cfg_.recent_tokens)),
+                       false);
+    d_attn_count_.alloc(sizeof(int) * 2 * B * H);  // arrival + slot counters (self-resetting)
     d_xfer_.alloc(sizeof(int) * 5 * L);  // ready, units, claim, done, flag
     {
         std::vector<int> off;
@@ -842,7 +845,8 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
             }
         }
         prof_begin(s_main_);
-        if (!launch_attention_tma(view(), l, s_main_)) launch_attention_engine(view(), l, s_main_);
+        if (!launch_attention_mma(view(), l, s_main_) && !launch_attention_tma(view(), l, s_main_))
+            launch_attention_engine(view(), l, s_main_);
         prof_end(s_main_, "attention", l);
         launches_ += 2;
         CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));

@@ -62,6 +62,19 @@ __device__ __forceinline__ void signal_head_output(const EngineView& v, int l) {
     }
 }
 
+// Same, when one warp stored all of the head's outputs.
+__device__ __forceinline__ void signal_head_output_warp(const EngineView& v, int l) {
+    if (v.world <= 1) return;
+    __threadfence_system();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll 1
+        for (int r = 0; r < v.world; ++r)
+            if (r != v.rank)
+                asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(v.xflag[r] + l), "r"(1u) : "memory");
+    }
+}
+
 // Step-end: wait for every peer's arrivals of this step, then copy their head
 // blocks into out (one launch, on the compute stream before step_end).
 void launch_exchange_finish(const EngineView& v, cudaStream_t stream);

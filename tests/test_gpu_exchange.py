@@ -2,8 +2,12 @@
 clo_engine_exchange_handle / clo_engine_attach_peers, csrc/exchange.cuh) on
 one B200: shard engines in one process (shared pointers) and in separate
 processes (CUDA IPC mappings of the same device) each produce the WHOLE
-model's outputs [B][L][hq][d], bit-identical to the unsharded engine's — the
-per-layer all-gather of SURVEY.md §8e without an NCCL launch. The world-size
+model's outputs [B][L][hq][d], equal to the unsharded engine's — the
+per-layer all-gather of SURVEY.md §8e without an NCCL launch. Selections and
+decisions are bit-identical; outputs agree to float rounding (the tensor-core
+kernel spreads a head's attend set over warps by the rank's own head count,
+so the partial-merge order differs between shardings; every configuration is
+bit-reproducible run to run, see test_outputs_bit_reproducible). The world-size
 2 host plumbing (handle exchange over torch.distributed) runs here exactly as
 it does across GPUs; only the peer mapping differs (same device vs NVLink)."""
 import ctypes as C
@@ -94,7 +98,7 @@ def _step_all(engines, t):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_in_process_shards_all_gather_bit_exact(world):
+def test_in_process_shards_all_gather(world):
     case = _case()
     want, heads = _unsharded(case)
     engines = [_shard_engine(case, world, r) for r in range(world)]
@@ -106,7 +110,7 @@ def test_in_process_shards_all_gather_bit_exact(world):
         outs = _step_all(eng, t)
         for r, out in enumerate(outs):
             assert np.isfinite(out).all(), f"rank {r} step {t}: exchange left holes"
-            np.testing.assert_array_equal(out, want[t - 1], err_msg=f"rank {r} step {t}")
+            np.testing.assert_allclose(out, want[t - 1], rtol=1e-5, atol=1e-6, err_msg=f"rank {r} step {t}")
     for (e, sh) in engines:  # selections and decisions of every shard = the unsharded ones
         for l in range(case["cfg"].shape.num_layers):
             for g in range(sh.n_kv):
@@ -173,7 +177,7 @@ def _ipc_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_processes_cuda_ipc_all_gather_bit_exact():
+def test_two_processes_cuda_ipc_all_gather():
     """Two processes, one shard each, handles exchanged over gloo, peer
     buffers mapped with cudaIpcOpenMemHandle: the multi-process protocol
     bench.py --config 4 uses across GPUs."""
@@ -195,4 +199,14 @@ def test_two_processes_cuda_ipc_all_gather_bit_exact():
         p.join(timeout=60)
         assert p.exitcode == 0
     for rank in range(2):
-        np.testing.assert_array_equal(got[rank], want)
+        np.testing.assert_allclose(got[rank], want, rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(got[0], got[1])  # every rank holds the same gathered outputs
+
+
+def test_outputs_bit_reproducible():
+    """Two engines on the same inputs: bit-identical outputs (the partial
+    merge order is fixed by the work decomposition, not by arrival order)."""
+    case = _case(steps=3)
+    a, _ = _unsharded(case)
+    b, _ = _unsharded(case)
+    np.testing.assert_array_equal(a, b)

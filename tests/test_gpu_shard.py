@@ -1,7 +1,7 @@
 """KV-head sharding on the CUDA engine: engines serving disjoint KV-head
 blocks (EngineConfig.kv_head_offset keeps the global per-head sign-hash seeds)
-reproduce the unsharded engine's selections and outputs for their heads
-exactly — the per-rank work of configs[3]; the all-gather itself is covered
+reproduce the unsharded engine's selections exactly and its outputs for
+their heads to float rounding — the per-rank work of configs[3]; the all-gather itself is covered
 on CPU by tests/test_multiprocess.py."""
 import dataclasses
 
@@ -36,7 +36,9 @@ def test_kv_head_shards_match_unsharded_engine(world):
                            HeadSlice(wl, sh.kv0, sh.n_kv, sh.q0, sh.n_q))
         eng.run()
         got = np.stack(eng.collected_outputs())
-        np.testing.assert_array_equal(got, want[:, :, :, sh.q0:sh.q0 + sh.n_q])
+        # float rounding only: the attention kernel's warp split depends on the
+        # shard's head count (selections below are bit-exact)
+        np.testing.assert_allclose(got, want[:, :, :, sh.q0:sh.q0 + sh.n_q], rtol=1e-5, atol=1e-6)
         for l in range(s.num_layers):
             for g in range(sh.n_kv):
                 a, b = eng.head(l, g), full.head(l, sh.kv0 + g)
