@@ -361,6 +361,33 @@ clo_status clo_plan_partition(const double* difficulty, int L, int H, double t_c
 uint64_t clo_cache_bytes(int offloaded_heads, int entry_k, int held_window_tokens, int num_layers,
                          int num_q_heads, int head_dim, int bytes_per_element);
 
+/* ------------------------------------------------------------------------ */
+/* Workload traces: the reference's wire format (trace_io.hpp:12-64,         */
+/* trace_io.cpp:83-266). Host functions; a trace is one sequence.            */
+typedef struct clo_trace clo_trace;
+/* read_trace (trace_io.cpp:129-183): validates magic, version, widths and
+ * trailing bytes the same way (CLO_ERR_IO / CLO_ERR_CONFIG). */
+clo_status clo_trace_open(const char* path, clo_trace** out);
+void clo_trace_close(clo_trace* t);
+clo_status clo_trace_info(const clo_trace* t, clo_model_shape* shape, int* n_prompt, int* n_steps,
+                          int* element_width);
+/* TraceSource::prompt_k/v (trace_io.cpp:230-236): n_prompt x d rows of
+ * (layer, kv_head) converted to `dtype` (bf16 RNE, f32 or f64). */
+clo_status clo_trace_prompt(const clo_trace* t, int layer, int kv_head, int dtype, void* k_out,
+                            void* v_out);
+/* TraceSource::true_query / approx_query / new_k_row / new_v_row
+ * (trace_io.cpp:238-266) of step t, in the engine's clo_step_io layout:
+ * true_q/approx_q [L][hq][d] f32 (approx = the layer l-1 hidden block, layer 0
+ * its own), new_k/new_v [L][hkv][d] of `dtype` (t >= 1). Any output may be NULL. */
+clo_status clo_trace_step(const clo_trace* t, int step, float* true_q, float* approx_q, void* new_k,
+                          void* new_v, int dtype);
+/* write_trace (trace_io.cpp:83-127) from arrays: prompt_k/v [L][hkv][n_prompt][d],
+ * true_q [n_steps+1][L][hq][d] (the hidden blocks), new_k/v [n_steps][L][hkv][d];
+ * element_width 4 or 8; also writes the <path>.json sidecar. */
+clo_status clo_trace_write(const char* path, const clo_model_shape* shape, int n_prompt, int n_steps,
+                           int element_width, const double* prompt_k, const double* prompt_v,
+                           const double* true_q, const double* new_k, const double* new_v);
+
 /* Build/diagnostic info: "sm_100a", ABI version, compiled kernels. */
 const char* clo_build_info(void);
 

@@ -336,6 +336,39 @@ class Reference(_Common):
                                                  _p(idx, C.c_int), _p(sc, C.c_double)))
         return idx, sc
 
+    # -- trace wire format (trace_io.cpp) -----------------------------------
+    def record_synthetic_trace(self, path, L, hq, hkv, d, n_prompt, steps, d_model=64, sigma_step=0.02,
+                               sigma_layer=0.01, seed=1, tie=False, width=8):
+        """The reference's SyntheticModel recorded with record_trace + write_trace."""
+        self._check(self.lib.ref_record_synthetic_trace(
+            C.c_int(L), C.c_int(hq), C.c_int(hkv), C.c_int(d), C.c_int(d_model), C.c_int(n_prompt),
+            C.c_int(steps), C.c_double(sigma_step), C.c_double(sigma_layer), C.c_uint64(seed),
+            C.c_int(int(tie)), C.c_int(width), str(path).encode()))
+
+    def read_trace(self, path):
+        """read_trace(path) -> (hdr, prompt [L][H][2][n][d], hidden [S+1][L][hq*d], step [S][L][2][H][d])."""
+        hdr = np.zeros(7, np.int32)
+        self._check(self.lib.ref_read_trace(str(path).encode(), _p(hdr, C.c_int), None, None, None))
+        L, hq, H, d, n, S, _ = (int(x) for x in hdr)
+        prompt = np.zeros((L, H, 2, n, d))
+        hidden = np.zeros((S + 1, L, hq * d))
+        step = np.zeros((max(S, 0), L, 2, H, d))
+        self._check(self.lib.ref_read_trace(str(path).encode(), _p(hdr, C.c_int), _p(prompt, C.c_double),
+                                            _p(hidden, C.c_double), _p(step, C.c_double)))
+        return hdr, prompt, hidden, step
+
+    def run_engine_trace(self, cfg: EngineCfg, tau, q_importance, persistent, path, json_cap=1 << 24):
+        """Reference DecodeEngine over TraceSource(read_trace(path)): (outputs, cache_state_json)."""
+        tau_ = np.ascontiguousarray(tau, np.float64)
+        qi = np.ascontiguousarray(q_importance, np.float64)
+        pers = np.ascontiguousarray(persistent, np.int32)
+        outs = np.zeros((max(cfg.steps, 1), cfg.num_layers, cfg.num_q_heads, cfg.head_dim))
+        buf = C.create_string_buffer(json_cap)
+        self._check(self.lib.ref_run_engine_trace(
+            C.byref(cfg), _p(tau_, C.c_double), _p(qi, C.c_double), _p(pers, C.c_int), str(path).encode(),
+            _p(outs, C.c_double), buf, C.c_size_t(json_cap)))
+        return outs, buf.value.decode()
+
     def run_engine(self, cfg: EngineCfg, tau, q_importance, persistent, prompt_k, prompt_v,
                    true_q, approx_q, new_k, new_v, json_cap=1 << 24):
         """Full reference DecodeEngine run; returns (outputs, cache_state_json, step_seconds)."""

@@ -24,6 +24,7 @@
 #include "kvsim/rng.hpp"
 #include "kvsim/similarity_cache.hpp"
 #include "kvsim/synthetic_model.hpp"
+#include "kvsim/trace_io.hpp"
 
 using namespace kvsim;
 
@@ -390,6 +391,99 @@ int ref_bench_units(const ref_engine_cfg* c, double tau, const double* q_importa
             return status[w];
         }
     return 0;
+}
+
+
+// --- trace wire format (trace_io.cpp) -------------------------------------
+// record_trace(SyntheticModel(cfg), width) + write_trace(path): a trace made
+// by the reference's own generator and writer.
+int ref_record_synthetic_trace(int L, int hq, int hkv, int d, int d_model, int n_prompt, int steps,
+                               double sigma_step, double sigma_layer, uint64_t seed, int tie, int width,
+                               const char* path) {
+    return guarded([&] {
+        SyntheticConfig cfg;
+        cfg.shape = ModelShape{L, hq, hkv, d, 2};
+        cfg.d_model = d_model;
+        cfg.n_prompt = n_prompt;
+        cfg.steps = steps;
+        cfg.sigma_step = sigma_step;
+        cfg.sigma_layer = sigma_layer;
+        cfg.seed = seed;
+        cfg.tie_layer_weights = tie != 0;
+        SyntheticModel model(cfg);
+        write_trace(path, record_trace(model, width));
+    });
+}
+
+// read_trace(path) widened to double in file order: hdr[7] = L, hq, hkv, d,
+// n_prompt, n_steps, width; prompt [L][hkv][2][n][d], hidden [S+1][L][hq*d],
+// step [S][L][2][hkv][d] (each may be NULL).
+int ref_read_trace(const char* path, int* hdr, double* prompt, double* hidden, double* step) {
+    return guarded([&] {
+        TraceData t = read_trace(path);
+        const int L = t.shape.num_layers, H = t.shape.num_kv_heads, d = t.shape.head_dim;
+        const int hq = t.shape.num_q_heads, n = t.n_prompt, S = t.n_steps;
+        const int h7[7] = {L, hq, H, d, n, S, t.element_width};
+        std::copy(h7, h7 + 7, hdr);
+        for (int l = 0; prompt && l < L; ++l)
+            for (int g = 0; g < H; ++g) {
+                double* o = prompt + ((size_t)l * H + g) * 2 * n * d;
+                std::copy(t.prompt_k[l][g].data.begin(), t.prompt_k[l][g].data.end(), o);
+                std::copy(t.prompt_v[l][g].data.begin(), t.prompt_v[l][g].data.end(), o + (size_t)n * d);
+            }
+        for (int s = 0; hidden && s <= S; ++s)
+            for (int l = 0; l < L; ++l)
+                std::copy(t.hidden[s][l].begin(), t.hidden[s][l].end(), hidden + ((size_t)s * L + l) * hq * d);
+        for (int s = 0; step && s < S; ++s)
+            for (int l = 0; l < L; ++l) {
+                double* o = step + ((size_t)s * L + l) * 2 * H * d;
+                std::copy(t.step_k[s][l].data.begin(), t.step_k[s][l].data.end(), o);
+                std::copy(t.step_v[s][l].data.begin(), t.step_v[s][l].data.end(), o + (size_t)H * d);
+            }
+    });
+}
+
+// DecodeEngine over TraceSource(read_trace(path)) — the reference replaying a
+// trace (c->n_prompt / c->steps are taken from the trace).
+int ref_run_engine_trace(const ref_engine_cfg* c, const double* tau, const double* q_importance,
+                         const int* persistent, const char* path, double* outputs, char* json_buf,
+                         size_t json_cap) {
+    return guarded([&] {
+        EngineConfig cfg = engine_config_of(c);
+        TraceSource src(read_trace(path));
+        const int L = c->num_layers, H = c->num_kv_heads, m = c->num_q_heads / c->num_kv_heads;
+        HeadProfiles profiles(L, std::vector<HeadProfileEntry>(H));
+        PartitionPlan plan;
+        plan.layers.resize(L);
+        for (int l = 0; l < L; ++l)
+            for (int g = 0; g < H; ++g) {
+                HeadProfileEntry& e = profiles[l][g];
+                e.q_importance.assign(q_importance + (static_cast<size_t>(l) * H + g) * m,
+                                      q_importance + (static_cast<size_t>(l) * H + g + 1) * m);
+                e.tau = tau[l * H + g];
+                if (persistent[l * H + g]) plan.layers[l].persistent_heads.push_back(g);
+            }
+        DecodeEngine engine(cfg, profiles, plan, src);
+        engine.prefill();
+        const int steps = src.decode_steps();
+        for (int t = 0; t < steps; ++t) engine.decode_step();
+        if (outputs) {
+            const auto& outs = engine.collected_outputs();
+            const int hq = c->num_q_heads, d = c->head_dim;
+            for (int t = 0; t < steps; ++t)
+                for (int l = 0; l < L; ++l)
+                    for (int h = 0; h < hq; ++h) {
+                        auto r = outs[t][l].row_span(h);
+                        std::copy(r.begin(), r.end(), outputs + ((static_cast<size_t>(t) * L + l) * hq + h) * d);
+                    }
+        }
+        if (json_buf && json_cap) {
+            std::string js = engine.cache_state_json();
+            size_t nn = std::min(js.size(), json_cap - 1);
+            std::memcpy(json_buf, js.data(), nn);
+            json_buf[nn] = 0;
+        }
+    });
 }
 
 }  // extern "C"

@@ -164,6 +164,12 @@ SIGNATURES = {
     "clo_compute_difficulty": (_I, [_D, _D, _D, C.POINTER(_D)]),
     "clo_plan_partition": (_I, [_P, _I, _I, _D, _D, _D, _U64, _U64, _P, C.POINTER(_I), C.POINTER(_I)]),
     "clo_cache_bytes": (_U64, [_I, _I, _I, _I, _I, _I, _I]),
+    "clo_trace_open": (_I, [C.c_char_p, C.POINTER(_P)]),
+    "clo_trace_close": (None, [_P]),
+    "clo_trace_info": (_I, [_P, C.POINTER(ModelShape), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+    "clo_trace_prompt": (_I, [_P, _I, _I, _I, _P, _P]),
+    "clo_trace_step": (_I, [_P, _I, _P, _P, _P, _P, _I]),
+    "clo_trace_write": (_I, [C.c_char_p, C.POINTER(ModelShape), _I, _I, _I, _P, _P, _P, _P, _P]),
     "clo_build_info": (C.c_char_p, []),
 }
 
