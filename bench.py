@@ -284,8 +284,9 @@ def run_ours(args):
     HQ, H = hs.n_q, hs.n_kv
     W, K = args.warmup, args.steps
     P = 2                       # profiled (instrumented-graph) steps
+    TL = 4                      # timeline steps (measured LayerTiming breakdown)
     E = 0 if args.no_e2e else K  # end-to-end (host buffers) steps
-    S = W + K + P + E + (W if E else 0)
+    S = W + K + P + TL + E + (W if E else 0)
     nmax = n + S
     dev = torch.device("cuda", local)
     gen = torch.Generator(device=dev)
@@ -440,6 +441,26 @@ def run_ours(args):
     prof_gathered = (pm1["gathered_bytes_device"] - pm0["gathered_bytes_device"]) / P
     prof_misses = (pm1["misses"] - pm0["misses"]) / P
 
+    # ---- measured LayerTiming breakdown (the reference's categories) --------
+    for _ in range(TL):
+        t_idx[0] += 1
+        io = dev_io(t_idx[0])
+        _lib.check(lib.clo_engine_timeline_step(eng.h, C.byref(io), C.c_void_p(sp)))
+    tl = eng.timeline()
+    tt = tl["totals"]
+    n_tl = max(1, tl["steps"])
+    layer_timing = {
+        "steps": tl["steps"],
+        "per_step_ms": {k[:-2]: round(1e3 * tt[k] / n_tl, 4) for k in
+                        ("compute_s", "transfer_s", "hidden_s", "exposed_s", "mgmt_s", "sync_s", "retrieval_s",
+                         "total_s", "wall_s")},
+        "share_of_total": {k[:-2]: round(tt[k] / tt["total_s"], 4) if tt["total_s"] else None for k in
+                           ("compute_s", "exposed_s", "mgmt_s", "sync_s", "retrieval_s")},
+        "note": "pipeline_sim.hpp LayerTiming categories measured with CUDA events in the production stream "
+                "layout; total = compute + exposed + mgmt + sync + retrieval (the reference's formula), "
+                "wall = measured compute-stream time",
+    }
+
     # ---- end-to-end through the C-ABI with pinned HOST buffers -------------
     e2e = None
     if E:
@@ -546,7 +567,7 @@ def run_ours(args):
             "pcie_gather_gbs_in_step": gathered / (ms / 1e3) / 1e9,
             "pcie_link_peak_gbs": best,
             "per_kernel_ms": {kk: round(v["ms"], 4) for kk, v in sorted(per_kernel.items())},
-            "roofline": roof, "rooflines": rooflines,
+            "roofline": roof, "rooflines": rooflines, "layer_timing": layer_timing,
             "e2e": e2e, "gpu_launches": launches, "kernels_per_step": eng.kernels_per_step(),
             "clocks": clocks.summary(), "cpu_baseline": cpu_baseline,
             "setup_s": setup_s, "prefill_s": prefill_s,

@@ -223,6 +223,38 @@ typedef struct clo_kernel_time {
 clo_status clo_engine_profile_step(clo_engine* e, const clo_step_io* io, void* stream,
                                    clo_kernel_time* out, int cap, int* count);
 
+/* Measured per-layer breakdown in the reference's LayerTiming categories
+ * (pipeline_sim.hpp:61-72; DecodeEngine::timeline() engine.hpp:105). The
+ * reference MODELS these times (schedule_layer, pipeline_sim.cpp:24-43);
+ * here they are CUDA-event timestamps of a decode step run through a copy of
+ * the step graph with the production stream layout:
+ *   compute   = append + attention of the layer
+ *   transfer  = the layer's zero-copy gather (raw, before overlap)
+ *   exposed   = time attention(l) waited for that gather after the compute
+ *               stream was ready; hidden = transfer - exposed
+ *   mgmt      = lookup (fused label refresh) + entry reconcile
+ *   retrieval = scoring + top-k selection
+ *   sync      = 0 (GPU-centric: no host round trip in the step)
+ *   total     = compute + exposed + mgmt + sync + retrieval (the reference's
+ *               formula, which serialises management and retrieval)
+ *   wall      = measured layer-to-layer time on the compute stream. */
+typedef struct clo_layer_timing {
+    int layer;
+    double compute_s, transfer_s, hidden_s, exposed_s, mgmt_s, sync_s, retrieval_s, total_s;
+    double wall_s;
+} clo_layer_timing;
+/* One decode step (clo_decode_step semantics) that also accumulates the
+ * timeline. Synchronous. */
+clo_status clo_engine_timeline_step(clo_engine* e, const clo_step_io* io, void* stream);
+/* PipelineTimeline: per_layer [cap >= L] summed over timeline steps, totals
+ * summed over layers (either may be NULL). */
+clo_status clo_get_timeline(clo_engine* e, clo_layer_timing* per_layer, int cap, clo_layer_timing* totals,
+                            uint64_t* steps);
+/* breakdown_to_json (pipeline_sim.cpp:115-135): {"steps", "layers": [...],
+ * "total"}, where "transfer_s" is the exposed transfer as in the reference,
+ * plus "transfer_raw_s" and "wall_s". */
+clo_status clo_timeline_json(clo_engine* e, char* buf, size_t cap, size_t* needed);
+
 /* Number of sm_100a kernels the engine enqueued since creation. */
 uint64_t clo_engine_kernel_launches(const clo_engine* e);
 /* Kernels per decode step (graph nodes that are kernels). */

@@ -113,6 +113,12 @@ class HeadState(C.Structure):
     ]
 
 
+class LayerTiming(C.Structure):  # clo_layer_timing (pipeline_sim.hpp:61-72 + wall_s)
+    _fields_ = [("layer", C.c_int)] + [(f, C.c_double) for f in (
+        "compute_s", "transfer_s", "hidden_s", "exposed_s", "mgmt_s", "sync_s", "retrieval_s", "total_s",
+        "wall_s")]
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("layer", C.c_int), ("ms", C.c_float)]
 
@@ -137,6 +143,9 @@ SIGNATURES = {
     "clo_get_entry_rows": (_I, [_P, _I, _I, _I, _P, _P]),
     "clo_cache_state_json": (_I, [_P, _I, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "clo_engine_profile_step": (_I, [_P, C.POINTER(StepIO), _P, C.POINTER(KernelTime), _I, C.POINTER(_I)]),
+    "clo_engine_timeline_step": (_I, [_P, C.POINTER(StepIO), _P]),
+    "clo_get_timeline": (_I, [_P, C.POINTER(LayerTiming), _I, C.POINTER(LayerTiming), C.POINTER(_U64)]),
+    "clo_timeline_json": (_I, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "clo_engine_kernel_launches": (_U64, [_P]),
     "clo_engine_kernels_per_step": (_I, [_P]),
     "clo_engine_exchange_handle": (_I, [_P, _I, _I, _P]),

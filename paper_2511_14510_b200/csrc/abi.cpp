@@ -194,6 +194,56 @@ clo_status clo_engine_profile_step(clo_engine* e, const clo_step_io* io, void* s
     });
 }
 
+clo_status clo_engine_timeline_step(clo_engine* e, const clo_step_io* io, void* stream) {
+    return guarded([&] {
+        if (!e || !io) fail(CLO_ERR_ARGUMENT, "null argument");
+        reinterpret_cast<Engine*>(e)->timeline_step(*io, static_cast<cudaStream_t>(stream));
+    });
+}
+
+clo_status clo_get_timeline(clo_engine* e, clo_layer_timing* per_layer, int cap, clo_layer_timing* totals,
+                            uint64_t* steps) {
+    return guarded([&] {
+        if (!e) fail(CLO_ERR_ARGUMENT, "null engine");
+        const Engine* en = reinterpret_cast<Engine*>(e);
+        const auto& tl = en->timeline();
+        const int L = en->config().shape.num_layers;
+        if (per_layer && cap < L) fail(CLO_ERR_ARGUMENT, "per_layer needs num_layers entries");
+        clo_layer_timing tot{};
+        tot.layer = -1;
+        for (int l = 0; l < L; ++l) {
+            clo_layer_timing t{};
+            t.layer = l;
+            if (!tl.empty()) t = tl[l];
+            if (per_layer) per_layer[l] = t;
+            tot.compute_s += t.compute_s;
+            tot.transfer_s += t.transfer_s;
+            tot.hidden_s += t.hidden_s;
+            tot.exposed_s += t.exposed_s;
+            tot.mgmt_s += t.mgmt_s;
+            tot.sync_s += t.sync_s;
+            tot.retrieval_s += t.retrieval_s;
+            tot.total_s += t.total_s;
+            tot.wall_s += t.wall_s;
+        }
+        if (totals) *totals = tot;
+        if (steps) *steps = en->timeline_steps();
+    });
+}
+
+clo_status clo_timeline_json(clo_engine* e, char* buf, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!e) fail(CLO_ERR_ARGUMENT, "null engine");
+        const std::string js = reinterpret_cast<Engine*>(e)->timeline_json();
+        if (needed) *needed = js.size() + 1;
+        if (buf && cap) {
+            const size_t n = std::min(js.size(), cap - 1);
+            std::memcpy(buf, js.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
 uint64_t clo_engine_kernel_launches(const clo_engine* e) {
     return reinterpret_cast<const Engine*>(e)->launches();
 }

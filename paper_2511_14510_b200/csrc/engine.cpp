@@ -144,14 +144,13 @@ Engine::~Engine() {
     cudaSetDevice(cfg_.device);
     for (int r = 0; r < kMaxRanks; ++r)
         if (xipc_[r]) cudaIpcCloseMemHandle(xbase_[r]);
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    if (graph_) cudaGraphDestroy(graph_);
-    if (pgraph_exec_) cudaGraphExecDestroy(pgraph_exec_);
-    if (pgraph_) cudaGraphDestroy(pgraph_);
-    for (auto& r : prof_) {
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
-    }
+    drop_graphs();
+    for (auto& recs : prof_)
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    if (tl_base_) cudaEventDestroy(tl_base_);
     for (auto ev : ev_attn_) cudaEventDestroy(ev);
     for (auto ev : ev_pref_) cudaEventDestroy(ev);
     for (auto ev : ev_sel_) cudaEventDestroy(ev);
@@ -445,22 +444,33 @@ SelArgs Engine::sel_args(int which, int layer) const {
 }
 
 void Engine::prof_begin(cudaStream_t st) {
-    if (!profiling_capture_) return;
-    if (prof_used_ == prof_.size()) {
+    if (capture_mode_ < 0) return;
+    auto& recs = prof_[capture_mode_];
+    size_t& used = prof_used_[capture_mode_];
+    if (used == recs.size()) {
         ProfRec r{};
         CLO_CUDA(cudaEventCreate(&r.a));
         CLO_CUDA(cudaEventCreate(&r.b));
-        prof_.push_back(r);
+        recs.push_back(r);
     }
-    CLO_CUDA(cudaEventRecordWithFlags(prof_[prof_used_].a, st, cudaEventRecordExternal));
+    CLO_CUDA(cudaEventRecordWithFlags(recs[used].a, st, cudaEventRecordExternal));
 }
 
 void Engine::prof_end(cudaStream_t st, const char* name, int layer) {
-    if (!profiling_capture_) return;
-    ProfRec& r = prof_[prof_used_++];
+    if (capture_mode_ < 0) return;
+    ProfRec& r = prof_[capture_mode_][prof_used_[capture_mode_]++];
     r.name = name;
     r.layer = layer;
     CLO_CUDA(cudaEventRecordWithFlags(r.b, st, cudaEventRecordExternal));
+}
+
+void Engine::drop_graphs() {  // views and pointers are baked into the graphs
+    for (int m = 0; m < kGraphModes; ++m) {
+        if (execs_[m]) cudaGraphExecDestroy(execs_[m]);
+        if (graphs_[m]) cudaGraphDestroy(graphs_[m]);
+        execs_[m] = nullptr;
+        graphs_[m] = nullptr;
+    }
 }
 
 void Engine::enqueue_select(int which, int layer, cudaStream_t st) {
@@ -555,18 +565,7 @@ void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_st
     seq_stride_ = seq_stride;
     layer_stride_ = layer_stride;
     head_stride_ = head_stride;
-    if (graph_exec_) {  // pointers are baked into the graph
-        cudaGraphExecDestroy(graph_exec_);
-        cudaGraphDestroy(graph_);
-        graph_exec_ = nullptr;
-        graph_ = nullptr;
-    }
-    if (pgraph_exec_) {
-        cudaGraphExecDestroy(pgraph_exec_);
-        cudaGraphDestroy(pgraph_);
-        pgraph_exec_ = nullptr;
-        pgraph_ = nullptr;
-    }
+    drop_graphs();  // pointers are baked into the graphs
 }
 
 namespace {
@@ -657,18 +656,7 @@ void Engine::attach_peers(const void* handles) {
         }
     }
     world_ = world;
-    for (auto* g : {&graph_, &pgraph_}) {  // views are baked into the graphs
-        if (*g) {
-            cudaGraphDestroy(*g);
-            *g = nullptr;
-        }
-    }
-    for (auto* x : {&graph_exec_, &pgraph_exec_}) {
-        if (*x) {
-            cudaGraphExecDestroy(*x);
-            *x = nullptr;
-        }
-    }
+    drop_graphs();
 }
 
 void Engine::set_desc(const StepDesc& d, cudaStream_t st) {
@@ -780,12 +768,16 @@ void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
     prefilled_ = true;
 }
 
-void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_t* exec_out) {
+void Engine::capture_graph(int mode) {
     const clo_model_shape& s = cfg_.shape;
     const int L = s.num_layers;
     const uint64_t before = launches_;
-    profiling_capture_ = profiled;
-    prof_used_ = 0;
+    const bool profiled = mode == kGraphSerial;
+    const bool flags = mode == kGraphProd && use_flag_transfer();
+    capture_mode_ = mode == kGraphProd ? -1 : mode;
+    prof_used_[mode] = 0;
+    cudaGraph_t* graph_out = &graphs_[mode];
+    cudaGraphExec_t* exec_out = &execs_[mode];
     // Three streams: selection (lookup + score/select of offloaded heads),
     // transfer (zero-copy gathers, back to back on the PCIe link) and compute
     // (persistent-head selection, append, attention). Work lists are per
@@ -796,13 +788,17 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
     cudaStream_t s_pref = profiled ? s_main_ : s_pref_;
     cudaStream_t s_xfer = profiled ? s_main_ : s_xfer_;
     CLO_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
+    if (mode == kGraphTimeline) {
+        if (!tl_base_) CLO_CUDA(cudaEventCreate(&tl_base_));
+        CLO_CUDA(cudaEventRecordWithFlags(tl_base_, s_main_, cudaEventRecordExternal));
+    }
     CLO_CUDA(cudaEventRecord(ev_fork_, s_main_));
     if (!profiled) {
         CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_fork_, 0));
         CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_fork_, 0));
         // one persistent transfer kernel per step streams every offloaded
         // layer's fetch list as soon as the selection stream publishes it
-        if (n_off_layers_ > 0 && use_flag_transfer()) {
+        if (n_off_layers_ > 0 && flags) {
             launch_gather_persistent(gather_args(0, 1), d_off_layers_.as<int>(), n_off_layers_,
                                      (int)gather_ctas(), s_xfer);
             launches_ += 1;
@@ -818,7 +814,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
             enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
             enqueue_select(1, l, s_pref);
             enqueue_reconcile(l, 0, s_pref);
-            if (profiled || !use_flag_transfer()) {
+            if (!flags) {
                 // one gather launch per layer, ordered by graph edges
                 CLO_CUDA(cudaEventRecord(ev_sel_[l], s_pref));
                 CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_sel_[l], 0));
@@ -837,7 +833,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         launch_append(view(), l, s_main_);
         prof_end(s_main_, "append", l);
         if (layer_has_off_[l]) {  // layer l's rows must be in HBM before its attention
-            if (!profiled && use_flag_transfer()) {
+            if (flags) {
                 launch_wait_flag(d_xfer_.as<int>() + 4 * cfg_.shape.num_layers + l, d_step_.as<int>(), s_main_);
                 launches_ += 1;
             } else {
@@ -866,7 +862,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
     CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
-    profiling_capture_ = false;
+    capture_mode_ = -1;
     CLO_CUDA(cudaGraphInstantiate(exec_out, *graph_out, 0));
     launches_ = before;  // captured launches are counted per replay
     size_t nn = 0;
@@ -879,7 +875,7 @@ void Engine::capture_graph(bool profiled, cudaGraph_t* graph_out, cudaGraphExec_
         CLO_CUDA(cudaGraphNodeGetType(nd, &t));
         kn += t == cudaGraphNodeTypeKernel;
     }
-    if (!profiled) kernels_per_step_ = kn;  // the production graph's kernel count
+    if (mode == kGraphProd) kernels_per_step_ = kn;  // the production graph's kernel count
 }
 
 StepDesc Engine::make_desc(const clo_step_io& io, cudaStream_t user) {
@@ -908,50 +904,152 @@ StepDesc Engine::make_desc(const clo_step_io& io, cudaStream_t user) {
     return desc;
 }
 
-std::vector<clo_kernel_time> Engine::profile_step(const clo_step_io& io, cudaStream_t user) {
-    if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
-    if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
-    CLO_CUDA(cudaSetDevice(cfg_.device));
-    const clo_model_shape& s = cfg_.shape;
-    set_desc(make_desc(io, user), user);
-    if (!pgraph_exec_) capture_graph(true, &pgraph_, &pgraph_exec_);
-    CLO_CUDA(cudaGraphLaunch(pgraph_exec_, user));
-    launches_ += kernels_per_step_;
-    if (io.on_host && io.out)
-        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * cfg_.batch * s.num_layers * world_ * s.num_q_heads * s.head_dim,
-                                 cudaMemcpyDeviceToHost, user));
-    ++steps_;
-    CLO_CUDA(cudaStreamSynchronize(user));
-    check_device_error();
-    std::vector<clo_kernel_time> out;
-    for (size_t i = 0; i < prof_used_; ++i) {
-        clo_kernel_time kt{};
-        std::snprintf(kt.name, sizeof kt.name, "%s", prof_[i].name);
-        kt.layer = prof_[i].layer;
-        CLO_CUDA(cudaEventElapsedTime(&kt.ms, prof_[i].a, prof_[i].b));
-        out.push_back(kt);
-    }
-    return out;
-}
-
-void Engine::decode_step(const clo_step_io& io, cudaStream_t user) {
+void Engine::launch_step(int mode, const clo_step_io& io, cudaStream_t user) {
     if (!prefilled_) fail(CLO_ERR_CONTRACT, "decode_step before prefill");
     if (steps_ >= cfg_.max_steps) fail(CLO_ERR_CONTRACT, "decode_step past the end of the workload");
     if (!io.true_q || !io.approx_q || !io.new_k || !io.new_v)
         fail(CLO_ERR_ARGUMENT, "step inputs must be non-null");
     CLO_CUDA(cudaSetDevice(cfg_.device));
     const clo_model_shape& s = cfg_.shape;
-    const int B = cfg_.batch, L = s.num_layers, HQ = s.num_q_heads, d = s.head_dim;
     set_desc(make_desc(io, user), user);
-    if (!graph_exec_) capture_graph(false, &graph_, &graph_exec_);
-    CLO_CUDA(cudaGraphLaunch(graph_exec_, user));
+    if (!execs_[mode]) capture_graph(mode);
+    CLO_CUDA(cudaGraphLaunch(execs_[mode], user));
     launches_ += kernels_per_step_;
     if (io.on_host && io.out)
-        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p, sizeof(float) * B * L * world_ * HQ * d, cudaMemcpyDeviceToHost,
-                                 user));
+        CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p,
+                                 sizeof(float) * cfg_.batch * s.num_layers * world_ * s.num_q_heads * s.head_dim,
+                                 cudaMemcpyDeviceToHost, user));
     CLO_CUDA(cudaGetLastError());
     ++steps_;
 }
+
+std::vector<clo_kernel_time> Engine::profile_step(const clo_step_io& io, cudaStream_t user) {
+    if (!execs_[kGraphProd] && prefilled_) capture_graph(kGraphProd);  // kernels_per_step_
+    launch_step(kGraphSerial, io, user);
+    CLO_CUDA(cudaStreamSynchronize(user));
+    check_device_error();
+    std::vector<clo_kernel_time> out;
+    const auto& recs = prof_[kGraphSerial];
+    for (size_t i = 0; i < prof_used_[kGraphSerial]; ++i) {
+        clo_kernel_time kt{};
+        std::snprintf(kt.name, sizeof kt.name, "%s", recs[i].name);
+        kt.layer = recs[i].layer;
+        CLO_CUDA(cudaEventElapsedTime(&kt.ms, recs[i].a, recs[i].b));
+        out.push_back(kt);
+    }
+    return out;
+}
+
+// Measured LayerTiming (pipeline_sim.hpp:61-72) of one step, from the
+// timeline graph's event timestamps (production streams, so overlap is real):
+//   compute   = append + attention           (the compute stream's own work)
+//   transfer  = the layer's zero-copy gather (raw, before overlap)
+//   exposed   = how long attention(l) waited for its gather after the compute
+//               stream was ready (append(l) done), capped at transfer
+//   hidden    = transfer - exposed          (overlapped with earlier layers)
+//   mgmt      = lookup (+ fused label refresh) + reconcile (entry bookkeeping)
+//   retrieval = scoring + top-k selection
+//   sync      = 0: GPU-centric, no host round trip inside the step
+//   total     = compute + exposed + mgmt + sync + retrieval (schedule_layer's
+//               formula, pipeline_sim.cpp:39); wall = the measured layer-to-
+//               layer time on the compute stream (selection and transfer
+//               overlap it, so wall < total when the pipeline works).
+void Engine::timeline_step(const clo_step_io& io, cudaStream_t user) {
+    if (!execs_[kGraphProd] && prefilled_) capture_graph(kGraphProd);
+    launch_step(kGraphTimeline, io, user);
+    CLO_CUDA(cudaStreamSynchronize(user));
+    check_device_error();
+    const int L = cfg_.shape.num_layers;
+    if (timeline_.empty()) {
+        timeline_.assign(L, clo_layer_timing{});
+        for (int l = 0; l < L; ++l) timeline_[l].layer = l;
+    }
+    struct Span {
+        double a = -1, b = -1;
+    };
+    auto at = [&](cudaEvent_t ev) {
+        float ms = 0.f;
+        CLO_CUDA(cudaEventElapsedTime(&ms, tl_base_, ev));
+        return (double)ms * 1e-3;
+    };
+    std::vector<std::array<double, 4>> dur(L);                    // compute, transfer, mgmt, retrieval
+    std::vector<Span> append(L), attn(L), gather(L);
+    for (auto& d : dur) d.fill(0.0);
+    const auto& recs = prof_[kGraphTimeline];
+    for (size_t i = 0; i < prof_used_[kGraphTimeline]; ++i) {
+        const ProfRec& r = recs[i];
+        if (r.layer < 0 || r.layer >= L) continue;
+        const double a = at(r.a), b = at(r.b), d = b - a;
+        const std::string n = r.name;
+        if (n == "append") {
+            dur[r.layer][0] += d;
+            append[r.layer] = {a, b};
+        } else if (n == "attention") {
+            dur[r.layer][0] += d;
+            attn[r.layer] = {a, b};
+        } else if (n == "gather_zero_copy") {
+            dur[r.layer][1] += d;
+            gather[r.layer] = {a, b};
+        } else if (n.rfind("lookup", 0) == 0 || n == "reconcile") {
+            dur[r.layer][2] += d;
+        } else if (n.rfind("select", 0) == 0) {
+            dur[r.layer][3] += d;
+        }
+    }
+    for (int l = 0; l < L; ++l) {
+        clo_layer_timing& t = timeline_[l];
+        const double transfer = dur[l][1];
+        double exposed = 0.0;
+        if (gather[l].b >= 0 && append[l].b >= 0 && attn[l].a >= 0)
+            exposed = std::min(transfer, std::max(0.0, attn[l].a - append[l].b));
+        t.compute_s += dur[l][0];
+        t.transfer_s += transfer;
+        t.exposed_s += exposed;
+        t.hidden_s += transfer - exposed;
+        t.mgmt_s += dur[l][2];
+        t.retrieval_s += dur[l][3];
+        t.total_s += dur[l][0] + exposed + dur[l][2] + dur[l][3];
+        const double prev = l > 0 ? attn[l - 1].b : 0.0;
+        t.wall_s += attn[l].b >= 0 ? attn[l].b - prev : 0.0;
+    }
+    ++timeline_steps_;
+}
+
+std::string Engine::timeline_json() const {
+    // breakdown_to_json's schema (pipeline_sim.cpp:115-135): "transfer_s" there
+    // is the EXPOSED transfer; raw transfer and the wall clock are extra keys.
+    char buf[64];
+    auto num = [&](double v) {
+        std::snprintf(buf, sizeof buf, "%.12g", v);
+        return std::string(buf);
+    };
+    auto row = [&](const clo_layer_timing& t) {
+        return "\"compute_s\": " + num(t.compute_s) + ", \"transfer_s\": " + num(t.exposed_s) +
+               ", \"hidden_s\": " + num(t.hidden_s) + ", \"mgmt_s\": " + num(t.mgmt_s) +
+               ", \"sync_s\": " + num(t.sync_s) + ", \"retrieval_s\": " + num(t.retrieval_s) +
+               ", \"total_s\": " + num(t.total_s) + ", \"transfer_raw_s\": " + num(t.transfer_s) +
+               ", \"wall_s\": " + num(t.wall_s);
+    };
+    clo_layer_timing tot{};
+    std::string out = "{\n  \"steps\": " + std::to_string(timeline_steps_) + ",\n  \"layers\": [";
+    for (size_t l = 0; l < timeline_.size(); ++l) {
+        const clo_layer_timing& t = timeline_[l];
+        out += (l ? ",\n    {" : "\n    {") + std::string("\"layer\": ") + std::to_string(t.layer) + ", " + row(t) + "}";
+        tot.compute_s += t.compute_s;
+        tot.transfer_s += t.transfer_s;
+        tot.hidden_s += t.hidden_s;
+        tot.exposed_s += t.exposed_s;
+        tot.mgmt_s += t.mgmt_s;
+        tot.sync_s += t.sync_s;
+        tot.retrieval_s += t.retrieval_s;
+        tot.total_s += t.total_s;
+        tot.wall_s += t.wall_s;
+    }
+    out += "\n  ],\n  \"total\": {" + row(tot) + "}\n}\n";
+    return out;
+}
+
+void Engine::decode_step(const clo_step_io& io, cudaStream_t user) { launch_step(kGraphProd, io, user); }
 
 void Engine::synchronize() {
     CLO_CUDA(cudaSetDevice(cfg_.device));

@@ -36,6 +36,13 @@ class Engine {
     // event-record nodes around every kernel, so per-launch device time is
     // measured inside the graph (bench roofline). Synchronous.
     std::vector<clo_kernel_time> profile_step(const clo_step_io& io, cudaStream_t user);
+    // One decode step through the timeline graph (production stream layout +
+    // event records): accumulates the measured per-layer breakdown in the
+    // reference's LayerTiming categories (pipeline_sim.hpp:61-86). Synchronous.
+    void timeline_step(const clo_step_io& io, cudaStream_t user);
+    const std::vector<clo_layer_timing>& timeline() const { return timeline_; }
+    uint64_t timeline_steps() const { return timeline_steps_; }
+    std::string timeline_json() const;
 
     // KV-head sharding: fused head-output all-gather over peer memory
     // (exchange.cuh). peer_handle() describes this engine's exchange buffer;
@@ -58,7 +65,10 @@ class Engine {
     void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
     void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
     GatherEngineArgs gather_args(int layer, int count_bytes) const;
-    void capture_graph(bool profiled, cudaGraph_t* graph, cudaGraphExec_t* exec);
+    enum GraphMode { kGraphProd = 0, kGraphSerial = 1, kGraphTimeline = 2, kGraphModes = 3 };
+    void capture_graph(int mode);
+    void drop_graphs();
+    void launch_step(int mode, const clo_step_io& io, cudaStream_t user);
     void prof_begin(cudaStream_t st);
     void prof_end(cudaStream_t st, const char* name, int layer);
     StepDesc make_desc(const clo_step_io& io, cudaStream_t user);
@@ -91,19 +101,19 @@ class Engine {
     cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_xfer_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr;
     std::vector<cudaEvent_t> ev_attn_, ev_pref_, ev_sel_;
-    cudaGraph_t graph_ = nullptr;
-    cudaGraphExec_t graph_exec_ = nullptr;
-    cudaGraph_t pgraph_ = nullptr;
-    cudaGraphExec_t pgraph_exec_ = nullptr;
-    bool profiling_capture_ = false;
+    std::array<cudaGraph_t, kGraphModes> graphs_{};
+    std::array<cudaGraphExec_t, kGraphModes> execs_{};
+    int capture_mode_ = -1;  // instrumented mode being captured (event records), -1 none
     struct ProfRec {
         cudaEvent_t a, b;
         const char* name;
         int layer;
     };
-    std::vector<ProfRec> prof_;
-    std::vector<cudaEvent_t> prof_pending_;
-    size_t prof_used_ = 0;
+    std::array<std::vector<ProfRec>, kGraphModes> prof_;
+    std::array<size_t, kGraphModes> prof_used_{};
+    cudaEvent_t tl_base_ = nullptr;           // timeline graph origin
+    std::vector<clo_layer_timing> timeline_;  // [L], summed over timeline steps
+    uint64_t timeline_steps_ = 0;
     StepDesc* desc_host_ = nullptr;
     std::vector<cudaEvent_t> desc_ev_;
     std::vector<int> desc_used_;

@@ -223,7 +223,9 @@ class DecodeEngine:
         q0 = np.ascontiguousarray(self.source.true_q[0], np.float32)
         check(self.lib.clo_prefill(self.h, ptr(q0), 1, None))
 
-    def decode_step(self):
+    def decode_step(self, timeline: bool = False):
+        """One decode step; timeline=True also measures the per-layer
+        LayerTiming breakdown (clo_engine_timeline_step)."""
         t = self.current_step + 1
         if t > self.source.steps:  # engine.cpp:226-228 (the C engine checks it too)
             raise _lib.ContractError("ContractError: decode_step past the end of the workload")
@@ -233,7 +235,8 @@ class DecodeEngine:
         s = self.cfg.shape
         out = np.empty((self.cfg.batch, s.num_layers, self.world * s.num_q_heads, s.head_dim), np.float32)
         io = _lib.StepIO(ptr(tq), ptr(aq), ptr(nk), ptr(nv), ptr(out), 1)
-        check(self.lib.clo_decode_step(self.h, C.byref(io), None))
+        step = self.lib.clo_engine_timeline_step if timeline else self.lib.clo_decode_step
+        check(step(self.h, C.byref(io), None))
         check(self.lib.clo_engine_synchronize(self.h))
         self.current_step = t
         if self.cfg.collect_outputs:
@@ -300,6 +303,24 @@ class DecodeEngine:
         blob = b"".join(handles)
         check(self.lib.clo_engine_attach_peers(self.h, blob))
         self.world = getattr(self, "_pending_world", len(handles))
+
+    def timeline(self) -> dict:
+        """DecodeEngine::timeline() (engine.hpp:105): PipelineTimeline of the
+        steps run with timeline=True, measured on the device."""
+        L = self.cfg.shape.num_layers
+        per = (_lib.LayerTiming * L)()
+        tot = _lib.LayerTiming()
+        steps = C.c_uint64()
+        check(self.lib.clo_get_timeline(self.h, per, L, C.byref(tot), C.byref(steps)))
+        row = lambda t: {f: getattr(t, f) for f, _ in _lib.LayerTiming._fields_}
+        return {"steps": steps.value, "per_layer": [row(t) for t in per], "totals": row(tot)}
+
+    def timeline_json(self) -> str:
+        need = C.c_size_t()
+        check(self.lib.clo_timeline_json(self.h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(self.lib.clo_timeline_json(self.h, buf, need.value, C.byref(need)))
+        return buf.value.decode()
 
     def kernel_launches(self) -> int:
         return self.lib.clo_engine_kernel_launches(self.h)

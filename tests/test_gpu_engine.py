@@ -124,3 +124,37 @@ def test_non_finite_step_input_raises_numeric_error():
     g.prefill()
     with pytest.raises(NumericError):
         g.decode_step()
+
+
+def test_timeline_breakdown_measured():
+    """Measured LayerTiming (clo_engine_timeline_step): the reference's
+    categories hold their identities (hidden + exposed = transfer, total =
+    compute + exposed + mgmt + sync + retrieval), the persistent layer 0
+    moves nothing, and timeline steps compute the same outputs as plain steps."""
+    import json as _json
+    from tests.engine_harness import make_case, gpu_engine
+    case = make_case(L=3, hq=8, hkv=2, d=128, n_prompt=700, steps=6, k=64, batch=2, kv_dtype="bf16",
+                     sink=4, recent=64, sigma_step=0.3)
+    a, b = gpu_engine(case), gpu_engine(case)
+    a.prefill()
+    b.prefill()
+    for t in range(case["wl"].steps):
+        oa = a.decode_step()
+        ob = b.decode_step(timeline=True)
+        np.testing.assert_array_equal(oa, ob)
+    tl = b.timeline()
+    assert tl["steps"] == case["wl"].steps
+    tot = tl["totals"]
+    for r in tl["per_layer"] + [tot]:
+        for f in ("compute_s", "transfer_s", "hidden_s", "exposed_s", "mgmt_s", "retrieval_s", "total_s", "wall_s"):
+            assert r[f] >= 0.0, f
+        assert r["sync_s"] == 0.0
+        assert abs(r["hidden_s"] + r["exposed_s"] - r["transfer_s"]) <= 1e-9
+        assert abs(r["compute_s"] + r["exposed_s"] + r["mgmt_s"] + r["sync_s"] + r["retrieval_s"]
+                   - r["total_s"]) <= 1e-9
+    assert tl["per_layer"][0]["transfer_s"] == 0.0  # layer 0 persistent: nothing gathered
+    assert tot["compute_s"] > 0 and tot["retrieval_s"] > 0 and tot["mgmt_s"] > 0
+    assert b.metrics()["misses"] > 0 and tot["transfer_s"] > 0
+    doc = _json.loads(b.timeline_json())
+    assert doc["steps"] == case["wl"].steps and len(doc["layers"]) == 3
+    assert abs(doc["total"]["transfer_s"] - tot["exposed_s"]) <= 1e-9  # the reference's key = exposed
