@@ -448,6 +448,9 @@ def run_ours(args):
         _lib.check(lib.clo_engine_timeline_step(eng.h, C.byref(io), C.c_void_p(sp)))
     tl = eng.timeline()
     tt = tl["totals"]
+    if os.environ.get("CLO_BENCH_SPANS"):  # Gantt dump of the last timeline step
+        with open(os.environ["CLO_BENCH_SPANS"], "w") as f:
+            json.dump(eng.timeline_spans(), f)
     n_tl = max(1, tl["steps"])
     layer_timing = {
         "steps": tl["steps"],

@@ -250,6 +250,14 @@ clo_status clo_engine_timeline_step(clo_engine* e, const clo_step_io* io, void* 
  * summed over layers (either may be NULL). */
 clo_status clo_get_timeline(clo_engine* e, clo_layer_timing* per_layer, int cap, clo_layer_timing* totals,
                             uint64_t* steps);
+/* Kernel spans of the most recent timeline step (start/end ms since the
+ * step's graph began; production stream layout, so spans overlap). */
+typedef struct clo_kernel_span {
+    char name[32];
+    int layer;
+    float start_ms, end_ms;
+} clo_kernel_span;
+clo_status clo_timeline_spans(clo_engine* e, clo_kernel_span* out, int cap, int* count);
 /* breakdown_to_json (pipeline_sim.cpp:115-135): {"steps", "layers": [...],
  * "total"}, where "transfer_s" is the exposed transfer as in the reference,
  * plus "transfer_raw_s" and "wall_s". */

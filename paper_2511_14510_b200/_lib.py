@@ -119,6 +119,10 @@ class LayerTiming(C.Structure):  # clo_layer_timing (pipeline_sim.hpp:61-72 + wa
         "wall_s")]
 
 
+class KernelSpan(C.Structure):  # clo_kernel_span
+    _fields_ = [("name", C.c_char * 32), ("layer", C.c_int), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("layer", C.c_int), ("ms", C.c_float)]
 
@@ -145,6 +149,7 @@ SIGNATURES = {
     "clo_engine_profile_step": (_I, [_P, C.POINTER(StepIO), _P, C.POINTER(KernelTime), _I, C.POINTER(_I)]),
     "clo_engine_timeline_step": (_I, [_P, C.POINTER(StepIO), _P]),
     "clo_get_timeline": (_I, [_P, C.POINTER(LayerTiming), _I, C.POINTER(LayerTiming), C.POINTER(_U64)]),
+    "clo_timeline_spans": (_I, [_P, C.POINTER(KernelSpan), _I, C.POINTER(_I)]),
     "clo_timeline_json": (_I, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "clo_engine_kernel_launches": (_U64, [_P]),
     "clo_engine_kernels_per_step": (_I, [_P]),

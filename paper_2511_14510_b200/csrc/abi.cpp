@@ -231,6 +231,15 @@ clo_status clo_get_timeline(clo_engine* e, clo_layer_timing* per_layer, int cap,
     });
 }
 
+clo_status clo_timeline_spans(clo_engine* e, clo_kernel_span* out, int cap, int* count) {
+    return guarded([&] {
+        if (!e) fail(CLO_ERR_ARGUMENT, "null engine");
+        const auto& sp = reinterpret_cast<Engine*>(e)->last_spans();
+        if (count) *count = (int)sp.size();
+        for (int i = 0; out && i < cap && i < (int)sp.size(); ++i) out[i] = sp[i];
+    });
+}
+
 clo_status clo_timeline_json(clo_engine* e, char* buf, size_t cap, size_t* needed) {
     return guarded([&] {
         if (!e) fail(CLO_ERR_ARGUMENT, "null engine");

@@ -1,5 +1,6 @@
 // encode.cu — K6 (prefill sign-hash encode), K5 (per-step append), helpers.
 #include "encode.cuh"
+#include "select.cuh"
 
 namespace clo {
 
@@ -105,7 +106,11 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
         for (int b0 = 0; b0 < v.words * 64; b0 += blockDim.x) {
             const int bit = b0 + threadIdx.x;
             double s = 0.0;
-            if (bit < v.bits)
+            if (bit < v.bits && v.d == 128) {
+                double s1[1] = {0.0};
+                signhash_chain<128, 1>(pt + bit, (size_t)v.bits, kd, 128, s1);
+                s = s1[0];
+            } else if (bit < v.bits)
                 for (int c0 = 0; c0 < v.d; c0 += 32) {  // 32 loads in flight, sequential chain
                     double p[32];
 #pragma unroll

@@ -299,7 +299,15 @@ void Engine::allocate() {
     }
 
     CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
-    CLO_CUDA(cudaStreamCreateWithFlags(&s_pref_, cudaStreamNonBlocking));
+    {
+        // The selection stream feeds the transfer stream: CLO_SEL_PRIO=high
+        // schedules its CTAs ahead of attention's (experiment switch).
+        const char* e = getenv("CLO_SEL_PRIO");
+        int lo = 0, hi = 0;
+        CLO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int p = e && std::string(e) == "high" ? hi : (e && std::string(e) == "mid" ? (lo + hi) / 2 : lo);
+        CLO_CUDA(cudaStreamCreateWithPriority(&s_pref_, cudaStreamNonBlocking, p));
+    }
     // The transfer stream gets the highest priority: when attention CTAs
     // retire, the next layer's gather CTAs are scheduled first so the PCIe
     // link does not idle behind compute.
@@ -976,10 +984,17 @@ void Engine::timeline_step(const clo_step_io& io, cudaStream_t user) {
     std::vector<Span> append(L), attn(L), gather(L);
     for (auto& d : dur) d.fill(0.0);
     const auto& recs = prof_[kGraphTimeline];
+    spans_.clear();
     for (size_t i = 0; i < prof_used_[kGraphTimeline]; ++i) {
         const ProfRec& r = recs[i];
-        if (r.layer < 0 || r.layer >= L) continue;
         const double a = at(r.a), b = at(r.b), d = b - a;
+        clo_kernel_span sp{};
+        std::snprintf(sp.name, sizeof sp.name, "%s", r.name);
+        sp.layer = r.layer;
+        sp.start_ms = (float)(a * 1e3);
+        sp.end_ms = (float)(b * 1e3);
+        spans_.push_back(sp);
+        if (r.layer < 0 || r.layer >= L) continue;
         const std::string n = r.name;
         if (n == "append") {
             dur[r.layer][0] += d;

@@ -43,6 +43,8 @@ class Engine {
     const std::vector<clo_layer_timing>& timeline() const { return timeline_; }
     uint64_t timeline_steps() const { return timeline_steps_; }
     std::string timeline_json() const;
+    // Kernel spans of the last timeline step: start/end ms since the step began.
+    const std::vector<clo_kernel_span>& last_spans() const { return spans_; }
 
     // KV-head sharding: fused head-output all-gather over peer memory
     // (exchange.cuh). peer_handle() describes this engine's exchange buffer;
@@ -114,6 +116,7 @@ class Engine {
     cudaEvent_t tl_base_ = nullptr;           // timeline graph origin
     std::vector<clo_layer_timing> timeline_;  // [L], summed over timeline steps
     uint64_t timeline_steps_ = 0;
+    std::vector<clo_kernel_span> spans_;
     StepDesc* desc_host_ = nullptr;
     std::vector<cudaEvent_t> desc_ev_;
     std::vector<int> desc_used_;

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
             sims[j] = 0.0;
             if (valid[j]) {
                 bool deg;
-                const double c = cosine_seq(q + j * v.d, lab_s + j * v.d, v.d, &deg);
+                const double c = cosine_any(q + j * v.d, lab_s + j * v.d, v.d, &deg);
                 sims[j] = c;
                 if (deg || c <= 0.0) atomicOr(&s_degenerate, 2);
             } else {

@@ -28,6 +28,33 @@ __device__ __forceinline__ double cosine_seq(const double* a, const double* b, i
     return fmin(fmax(v, -1.0), 1.0);
 }
 
+// Same chains for a compile-time length, fully unrolled: the products are
+// independent of the accumulators, so only the three DADD chains are serial.
+template <int D>
+__device__ __forceinline__ double cosine_seq_d(const double* a, const double* b, bool* degenerate) {
+    double ab = 0.0, aa = 0.0, bb = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double x = a[i], y = b[i];
+        ab = dmac(ab, x, y);
+        aa = dmac(aa, x, x);
+        bb = dmac(bb, y, y);
+    }
+    if (aa == 0.0 || bb == 0.0) {
+        *degenerate = true;
+        return 0.0;
+    }
+    *degenerate = false;
+    double v = __ddiv_rn(ab, __dmul_rn(__dsqrt_rn(aa), __dsqrt_rn(bb)));
+    return fmin(fmax(v, -1.0), 1.0);
+}
+
+__device__ __forceinline__ double cosine_any(const double* a, const double* b, int n, bool* degenerate) {
+    if (n == 128) return cosine_seq_d<128>(a, b, degenerate);
+    if (n == 64) return cosine_seq_d<64>(a, b, degenerate);
+    return cosine_seq(a, b, n, degenerate);
+}
+
 // aggregate_similarity (similarity_cache.cpp:10-27); callers guarantee
 // non-negative weights and positive sims.
 __device__ __forceinline__ double aggregate_seq(const double* sims, const double* w, int m) {

@@ -59,9 +59,51 @@ void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, 
 // summed sequentially in IEEE double. Called by a whole CTA (blockDim.x a
 // multiple of 32). q64 [M][d] (smem), proj_t [d][bits] -> qbits [M][words].
 // M is a template parameter so no FP64 work is issued for absent members.
+// Sequential sign-hash dot products for a compile-time head dim: s_j +=
+// P^T[c][b] * q_j[c] for c = 0..D-1 in source order (separately rounded
+// multiply and add, bit-exact with the reference's scalar loop). Fully
+// unrolled, no bounds predicates, 16 P^T loads in flight per batch; the
+// products do not depend on the accumulators, so only the DADD chain is
+// serial.
+template <int D, int M>
+__device__ __forceinline__ void signhash_chain(const double* __restrict__ col, size_t stride, const double* q,
+                                               int qstride, double (&s)[M]) {
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 16) {
+        double p[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[i] = __ldg(col + (size_t)(c0 + i) * stride);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) s[j] = dmac(s[j], p[i], q[j * qstride + c0 + i]);
+    }
+}
+
+template <int M, int D>
+__device__ __forceinline__ void hash_queries_block_md(const double* q64, const double* proj_t, int bits, int words,
+                                                      uint64_t* qbits_out) {
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(qbits_out);
+    const int total = words * 64;
+    for (int b0 = 0; b0 < total; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        double s[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) s[j] = 0.0;
+        if (b < bits) signhash_chain<D, M>(proj_t + b, (size_t)bits, q64, D, s);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const unsigned bal = __ballot_sync(0xffffffffu, b < bits && s[j] >= 0.0);
+            if ((threadIdx.x & 31) == 0 && b < total) out32[j * words * 2 + (b >> 5)] = bal;
+        }
+    }
+}
+
 template <int M>
 __device__ __forceinline__ void hash_queries_block_m(const double* q64, int d, const double* proj_t,
                                                      int bits, int words, uint64_t* qbits_out) {
+    if (d == 128) return hash_queries_block_md<M, 128>(q64, proj_t, bits, words, qbits_out);
+    if (d == 64) return hash_queries_block_md<M, 64>(q64, proj_t, bits, words, qbits_out);
     uint32_t* out32 = reinterpret_cast<uint32_t*>(qbits_out);
     const int total = words * 64;
     for (int b0 = 0; b0 < total; b0 += blockDim.x) {

@@ -315,6 +315,14 @@ class DecodeEngine:
         row = lambda t: {f: getattr(t, f) for f, _ in _lib.LayerTiming._fields_}
         return {"steps": steps.value, "per_layer": [row(t) for t in per], "totals": row(tot)}
 
+    def timeline_spans(self) -> list:
+        """(name, layer, start_ms, end_ms) of every kernel of the last timeline step."""
+        cnt = C.c_int()
+        check(self.lib.clo_timeline_spans(self.h, None, 0, C.byref(cnt)))
+        buf = (_lib.KernelSpan * max(1, cnt.value))()
+        check(self.lib.clo_timeline_spans(self.h, buf, cnt.value, C.byref(cnt)))
+        return [(s.name.decode(), s.layer, s.start_ms, s.end_ms) for s in buf[:cnt.value]]
+
     def timeline_json(self) -> str:
         need = C.c_size_t()
         check(self.lib.clo_timeline_json(self.h, None, 0, C.byref(need)))
