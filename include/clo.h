@@ -421,12 +421,43 @@ clo_status clo_trace_prompt(const clo_trace* t, int layer, int kv_head, int dtyp
  * its own), new_k/new_v [L][hkv][d] of `dtype` (t >= 1). Any output may be NULL. */
 clo_status clo_trace_step(const clo_trace* t, int step, float* true_q, float* approx_q, void* new_k,
                           void* new_v, int dtype);
+/* The raw hidden block [hq][d] (float64) of (step, layer): TraceSource::true_query's
+ * values before any narrowing. */
+clo_status clo_trace_hidden(const clo_trace* t, int step, int layer, double* out);
 /* write_trace (trace_io.cpp:83-127) from arrays: prompt_k/v [L][hkv][n_prompt][d],
  * true_q [n_steps+1][L][hq][d] (the hidden blocks), new_k/v [n_steps][L][hkv][d];
  * element_width 4 or 8; also writes the <path>.json sidecar. */
 clo_status clo_trace_write(const char* path, const clo_model_shape* shape, int n_prompt, int n_steps,
                            int element_width, const double* prompt_k, const double* prompt_v,
                            const double* true_q, const double* new_k, const double* new_v);
+
+/* ------------------------------------------------------------------------ */
+/* Head profiling (profile_heads, profiler.cpp:19-125; head_profile.hpp:16-75) */
+typedef struct clo_profiler_config { /* ProfilerInputs, profiler.hpp:12-27 */
+    int blend_sequences; /* default 1: the blend fit uses the first N sources */
+    int blend_steps;     /* default 8 */
+    int topk;            /* target selection size for the blend fit, default 1 */
+    int sink_tokens;     /* default 4 */
+    int recent_tokens;   /* default 64 */
+    double eta, p, epsilon; /* defaults 0.8, 3.0, 0.1 */
+} clo_profiler_config;
+void clo_profiler_config_defaults(clo_profiler_config* cfg);
+/* HeadProfileEntry (head_profile.hpp:16-23); q_importance has m valid entries. */
+typedef struct clo_head_profile {
+    double q_importance[16];
+    double kv_importance, s_hat, tau, difficulty;
+    int placement; /* clo_placement: always OFFLOADED here (plan_partition assigns) */
+} clo_head_profile;
+/* profile_heads over probe traces: s_hat = mean adjacent-step cosine of the
+ * true queries; importance alpha per query head = clamp(sum (topk - stream)
+ * (full - stream) / sum (full - stream)^2, 0, 1) over the first blend_steps
+ * steps of the first blend_sequences sources, where full / streaming / top-k
+ * attention (exact top-k of cfg->topk keys) run on the GPU in float64 over
+ * the prompt rows; then kv_importance = max, s_hat = min over the group, tau,
+ * difficulty. provided_importance [L][hkv][m] (nullable) replaces the fit.
+ * out [L*hkv]. Synchronous. */
+clo_status clo_profile_heads(const clo_trace* const* sources, int n_sources, const clo_profiler_config* cfg,
+                             const double* provided_importance, clo_head_profile* out);
 
 /* Build/diagnostic info: "sm_100a", ABI version, compiled kernels. */
 const char* clo_build_info(void);

@@ -357,6 +357,25 @@ class Reference(_Common):
                                             _p(hidden, C.c_double), _p(step, C.c_double)))
         return hdr, prompt, hidden, step
 
+    def profile_heads(self, paths, blend_sequences=1, blend_steps=8, topk=1, sink=4, recent=64, eta=0.8, p=3.0,
+                      epsilon=0.1, provided=None):
+        """profile_heads over TraceSources: dict of q_importance [L][H][m], kv_importance, s_hat, tau,
+        difficulty [L][H]."""
+        hdr = self.read_trace(paths[0])[0]
+        L, hq, H = int(hdr[0]), int(hdr[1]), int(hdr[2])
+        m = hq // H
+        arr = (C.c_char_p * len(paths))(*[str(x).encode() for x in paths])
+        qi = np.zeros((L, H, m))
+        out = {k: np.zeros((L, H)) for k in ("kv_importance", "s_hat", "tau", "difficulty")}
+        prov = None if provided is None else np.ascontiguousarray(provided, np.float64)
+        self._check(self.lib.ref_profile_heads(
+            arr, C.c_int(len(paths)), C.c_int(blend_sequences), C.c_int(blend_steps), C.c_int(topk), C.c_int(sink),
+            C.c_int(recent), C.c_double(eta), C.c_double(p), C.c_double(epsilon),
+            None if prov is None else _p(prov, C.c_double), _p(qi, C.c_double),
+            *[_p(out[k], C.c_double) for k in ("kv_importance", "s_hat", "tau", "difficulty")]))
+        out["q_importance"] = qi
+        return out
+
     def run_engine_trace(self, cfg: EngineCfg, tau, q_importance, persistent, path, json_cap=1 << 24):
         """Reference DecodeEngine over TraceSource(read_trace(path)): (outputs, cache_state_json)."""
         tau_ = np.ascontiguousarray(tau, np.float64)

@@ -9,6 +9,7 @@
 // status codes of errors.hpp:10-41.
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -25,6 +26,7 @@
 #include "kvsim/similarity_cache.hpp"
 #include "kvsim/synthetic_model.hpp"
 #include "kvsim/trace_io.hpp"
+#include "kvsim/profiler.hpp"
 
 using namespace kvsim;
 
@@ -483,6 +485,49 @@ int ref_run_engine_trace(const ref_engine_cfg* c, const double* tau, const doubl
             std::memcpy(json_buf, js.data(), nn);
             json_buf[nn] = 0;
         }
+    });
+}
+
+
+// profile_heads (profiler.cpp:19-125) over TraceSources of the given trace
+// files. provided [L][H][m] may be NULL (blend fit). Outputs: q_importance
+// [L][H][m], kv_importance / s_hat / tau / difficulty [L][H].
+int ref_profile_heads(const char* const* paths, int n_paths, int blend_sequences, int blend_steps, int topk,
+                      int sink, int recent, double eta, double p, double epsilon, const double* provided,
+                      double* q_importance, double* kv_importance, double* s_hat, double* tau, double* difficulty) {
+    return guarded([&] {
+        std::vector<std::unique_ptr<TraceSource>> owned;
+        ProfilerInputs in;
+        for (int i = 0; i < n_paths; ++i) {
+            owned.push_back(std::make_unique<TraceSource>(read_trace(paths[i])));
+            in.sources.push_back(owned.back().get());
+        }
+        in.blend_sequences = blend_sequences;
+        in.blend_steps = blend_steps;
+        in.topk = topk;
+        in.sink_tokens = sink;
+        in.recent_tokens = recent;
+        in.eta = eta;
+        in.p = p;
+        in.epsilon = epsilon;
+        const ModelShape& sh = owned.front()->shape();
+        const int L = sh.num_layers, H = sh.num_kv_heads, m = sh.num_q_heads / sh.num_kv_heads;
+        if (provided) {
+            in.provided_importance.assign(L, std::vector<std::vector<double>>(H, std::vector<double>(m)));
+            for (int l = 0; l < L; ++l)
+                for (int g = 0; g < H; ++g)
+                    for (int j = 0; j < m; ++j) in.provided_importance[l][g][j] = provided[((size_t)l * H + g) * m + j];
+        }
+        HeadProfiles prof = profile_heads(in);
+        for (int l = 0; l < L; ++l)
+            for (int g = 0; g < H; ++g) {
+                const HeadProfileEntry& e = prof[l][g];
+                for (int j = 0; j < m; ++j) q_importance[((size_t)l * H + g) * m + j] = e.q_importance[j];
+                kv_importance[l * H + g] = e.kv_importance;
+                s_hat[l * H + g] = e.s_hat;
+                tau[l * H + g] = e.tau;
+                difficulty[l * H + g] = e.difficulty;
+            }
     });
 }
 

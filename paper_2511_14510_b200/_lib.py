@@ -119,6 +119,17 @@ class LayerTiming(C.Structure):  # clo_layer_timing (pipeline_sim.hpp:61-72 + wa
         "wall_s")]
 
 
+class ProfilerConfig(C.Structure):  # clo_profiler_config
+    _fields_ = [("blend_sequences", C.c_int), ("blend_steps", C.c_int), ("topk", C.c_int),
+                ("sink_tokens", C.c_int), ("recent_tokens", C.c_int),
+                ("eta", C.c_double), ("p", C.c_double), ("epsilon", C.c_double)]
+
+
+class HeadProfileC(C.Structure):  # clo_head_profile
+    _fields_ = [("q_importance", C.c_double * 16), ("kv_importance", C.c_double), ("s_hat", C.c_double),
+                ("tau", C.c_double), ("difficulty", C.c_double), ("placement", C.c_int)]
+
+
 class KernelSpan(C.Structure):  # clo_kernel_span
     _fields_ = [("name", C.c_char * 32), ("layer", C.c_int), ("start_ms", C.c_float), ("end_ms", C.c_float)]
 
@@ -183,6 +194,9 @@ SIGNATURES = {
     "clo_trace_info": (_I, [_P, C.POINTER(ModelShape), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "clo_trace_prompt": (_I, [_P, _I, _I, _I, _P, _P]),
     "clo_trace_step": (_I, [_P, _I, _P, _P, _P, _P, _I]),
+    "clo_trace_hidden": (_I, [_P, _I, _I, _P]),
+    "clo_profiler_config_defaults": (None, [C.POINTER(ProfilerConfig)]),
+    "clo_profile_heads": (_I, [_P, _I, C.POINTER(ProfilerConfig), _P, _P]),
     "clo_trace_write": (_I, [C.c_char_p, C.POINTER(ModelShape), _I, _I, _I, _P, _P, _P, _P, _P]),
     "clo_build_info": (C.c_char_p, []),
 }

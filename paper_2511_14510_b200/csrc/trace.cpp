@@ -187,6 +187,16 @@ clo_status clo_trace_step(const clo_trace* t, int step, float* true_q, float* ap
     });
 }
 
+clo_status clo_trace_hidden(const clo_trace* t, int step, int layer, double* out) {
+    return guarded([&] {
+        if (!t || !out) fail(CLO_ERR_ARGUMENT, "null argument");
+        if (step < 0 || step > t->n_steps) fail(CLO_ERR_INDEX, "trace step out of range");
+        if (layer < 0 || layer >= t->shape.num_layers) fail(CLO_ERR_INDEX, "trace layer out of range");
+        const size_t blk = hq_d(*t);
+        std::memcpy(out, t->hidden.data() + ((size_t)step * t->shape.num_layers + layer) * blk, blk * sizeof(double));
+    });
+}
+
 clo_status clo_trace_write(const char* path, const clo_model_shape* shape, int n_prompt, int n_steps,
                            int element_width, const double* prompt_k, const double* prompt_v, const double* true_q,
                            const double* new_k, const double* new_v) {
