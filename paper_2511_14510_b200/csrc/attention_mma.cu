@@ -259,8 +259,9 @@ __device__ __noinline__ void combine_head(const EngineView& v, int l, int t, int
     signal_head_output_warp(v, l);
 }
 
-template <int D, int M, int kWarpsM, int kStagesM, int kCtasPerSM, int kTileM>
-__global__ void __launch_bounds__(kWarpsM * 32, kCtasPerSM) attn_mma_stream_kernel(const __grid_constant__ EngineView v, int l, const __grid_constant__ MmaPlan pl,
+template <int D, int M, int kWarpsM, int kStagesM, int kCtasPerSM, int kTileM, int kRegCap>
+// kRegCap: see launch_mma_shape.
+__global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constant__ EngineView v, int l, const __grid_constant__ MmaPlan pl,
                                                                        float* part) {
     using T = __nv_bfloat16;
     constexpr uint32_t kRowBytes = D * 2;
@@ -602,18 +603,34 @@ MmaShape mma_shape() {
     return sh;
 }
 
-template <int D, int M, int W, int S, int C, int TM>
-void launch_mma_shape(const EngineView& v, int layer, cudaStream_t stream) {
+template <int D, int M, int W, int S, int C, int TM, int RC>
+void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
     const MmaPlan pl = make_plan(v, W, C, TM);
     const size_t ring = (size_t)W * S * 2 * TM * (D * 2 + 16);
     const size_t sm = ring + (size_t)pl.R * M * D * sizeof(float);  // + staged queries
     static size_t configured = 0;
     if (sm > configured) {
-        cudaFuncSetAttribute(attn_mma_stream_kernel<D, M, W, S, C, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
+        cudaFuncSetAttribute(attn_mma_stream_kernel<D, M, W, S, C, TM, RC>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         configured = sm;
     }
-    attn_mma_stream_kernel<D, M, W, S, C, TM><<<pl.G, W * 32, sm, stream>>>(v, layer, pl, v.attn_part);
+    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(v, layer, pl, v.attn_part);
+}
+
+// Register cap: CLO_ATTN_REGCAP=184 lets an 8-warp CTA share its SM with a
+// zero-copy gather CTA. Measured on B200 that slows the step by ~12%: the
+// gather's PCIe reads need their warps issued promptly, and a co-resident
+// attention CTA delays them (profiles/r1_attention_mma.md). Default: no cap.
+template <int D, int M, int W, int S, int C, int TM>
+void launch_mma_shape(const EngineView& v, int layer, cudaStream_t stream) {
+    static const bool capped = [] {
+        const char* e = getenv("CLO_ATTN_REGCAP");
+        return e && atoi(e) > 0 && atoi(e) < 255;
+    }();
+    if (capped)
+        launch_mma_shape_rc<D, M, W, S, C, TM, 184>(v, layer, stream);
+    else
+        launch_mma_shape_rc<D, M, W, S, C, TM, 255>(v, layer, stream);
 }
 
 template <int D, int M>
