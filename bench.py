@@ -259,6 +259,7 @@ def run_ours(args):
     world, rank, local = dist_env()
     if args.same_device:  # functional multi-rank check on a 1-GPU box (not a bench number)
         local = 0
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

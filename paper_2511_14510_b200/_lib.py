@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libclo.so")
+LIB_PATH = os.environ.get("CLO_LIB") or os.path.join(HERE, "libclo.so")  # CLO_LIB: A/B builds
 
 # clo_status (errors.hpp:10-41 taxonomy)
 STATUS_NAMES = {

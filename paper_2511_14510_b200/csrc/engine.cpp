@@ -160,6 +160,11 @@ Engine::~Engine() {
     if (s_main_) cudaStreamDestroy(s_main_);
     if (s_pref_) cudaStreamDestroy(s_pref_);
     if (s_xfer_) cudaStreamDestroy(s_xfer_);
+    if (s_copy_) cudaStreamDestroy(s_copy_);
+    for (int i = 0; i < 2; ++i) {
+        if (ev_in_[i]) cudaEventDestroy(ev_in_[i]);
+        if (ev_free_[i]) cudaEventDestroy(ev_free_[i]);
+    }
     if (desc_host_) cudaFreeHost(desc_host_);
     for (auto ev : desc_ev_) cudaEventDestroy(ev);
 }
@@ -254,6 +259,7 @@ void Engine::allocate() {
     d_in_aq_.alloc(sizeof(float) * B * L * HQ * d, false);
     d_in_nk_.alloc(esz * B * L * H * d, false);
     d_in_nv_.alloc(esz * B * L * H * d, false);
+    for (auto& b : d_in_) b.alloc(2 * sizeof(float) * B * L * HQ * d + 2 * esz * B * L * H * d, false);
     d_out_.alloc(sizeof(float) * B * L * HQ * d, false);
 
     for (int i = 0; i < 2; ++i) {
@@ -865,7 +871,7 @@ void Engine::capture_graph(int mode) {
         prof_begin(s_main_);
         launch_exchange_finish(view(), s_main_);
         prof_end(s_main_, "exchange_finish", -1);
-        launches_ += 1;
+        launches_ += 2;
     }
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
@@ -892,15 +898,33 @@ StepDesc Engine::make_desc(const clo_step_io& io, cudaStream_t user) {
     const size_t esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
     StepDesc desc{};
     if (io.on_host) {
+        // Inputs go through a double-buffered staging slot on the copy stream:
+        // this step's H2D overlaps the previous step's graph (only the graph
+        // that read this slot two steps ago must have finished), and the
+        // step's graph waits for its own copies.
         const size_t qb = sizeof(float) * B * L * HQ * d, kb = esz * B * L * H * d;
-        CLO_CUDA(cudaMemcpyAsync(d_in_tq_.p, io.true_q, qb, cudaMemcpyHostToDevice, user));
-        CLO_CUDA(cudaMemcpyAsync(d_in_aq_.p, io.approx_q, qb, cudaMemcpyHostToDevice, user));
-        CLO_CUDA(cudaMemcpyAsync(d_in_nk_.p, io.new_k, kb, cudaMemcpyHostToDevice, user));
-        CLO_CUDA(cudaMemcpyAsync(d_in_nv_.p, io.new_v, kb, cudaMemcpyHostToDevice, user));
-        desc.true_q = d_in_tq_.as<float>();
-        desc.approx_q = d_in_aq_.as<float>();
-        desc.new_k = d_in_nk_.p;
-        desc.new_v = d_in_nv_.p;
+        if (!s_copy_) {  // created on first host-buffer step: device-I/O engines keep 3 streams
+            CLO_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                CLO_CUDA(cudaEventCreateWithFlags(&ev_in_[i], cudaEventDisableTiming));
+                CLO_CUDA(cudaEventCreateWithFlags(&ev_free_[i], cudaEventDisableTiming));
+            }
+        }
+        const int slot = in_slot_;
+        in_slot_ ^= 1;
+        if (in_used_[slot]) CLO_CUDA(cudaStreamWaitEvent(s_copy_, ev_free_[slot], 0));
+        char* base = d_in_[slot].as<char>();
+        CLO_CUDA(cudaMemcpyAsync(base, io.true_q, qb, cudaMemcpyHostToDevice, s_copy_));
+        CLO_CUDA(cudaMemcpyAsync(base + qb, io.approx_q, qb, cudaMemcpyHostToDevice, s_copy_));
+        CLO_CUDA(cudaMemcpyAsync(base + 2 * qb, io.new_k, kb, cudaMemcpyHostToDevice, s_copy_));
+        CLO_CUDA(cudaMemcpyAsync(base + 2 * qb + kb, io.new_v, kb, cudaMemcpyHostToDevice, s_copy_));
+        CLO_CUDA(cudaEventRecord(ev_in_[slot], s_copy_));
+        CLO_CUDA(cudaStreamWaitEvent(user, ev_in_[slot], 0));
+        pending_free_ = slot;
+        desc.true_q = reinterpret_cast<const float*>(base);
+        desc.approx_q = reinterpret_cast<const float*>(base + qb);
+        desc.new_k = base + 2 * qb;
+        desc.new_v = base + 2 * qb + kb;
         desc.out = d_out_.as<float>();
     } else {
         desc.true_q = io.true_q;
@@ -923,6 +947,11 @@ void Engine::launch_step(int mode, const clo_step_io& io, cudaStream_t user) {
     if (!execs_[mode]) capture_graph(mode);
     CLO_CUDA(cudaGraphLaunch(execs_[mode], user));
     launches_ += kernels_per_step_;
+    if (pending_free_ >= 0) {  // the staging slot is reusable once this graph is done
+        CLO_CUDA(cudaEventRecord(ev_free_[pending_free_], user));
+        in_used_[pending_free_] = true;
+        pending_free_ = -1;
+    }
     if (io.on_host && io.out)
         CLO_CUDA(cudaMemcpyAsync(io.out, d_out_.p,
                                  sizeof(float) * cfg_.batch * s.num_layers * world_ * s.num_q_heads * s.head_dim,

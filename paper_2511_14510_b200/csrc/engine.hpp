@@ -97,6 +97,14 @@ class Engine {
     DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_, d_xfer_, d_off_layers_;
     int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
+    // host-input staging, double-buffered: step t+1's H2D copies run on a copy
+    // stream while step t's graph still executes
+    std::array<DevBuf, 2> d_in_;
+    int in_slot_ = 0;
+    cudaStream_t s_copy_ = nullptr;
+    std::array<cudaEvent_t, 2> ev_in_{}, ev_free_{};
+    std::array<bool, 2> in_used_{};
+    int pending_free_ = -1;  // slot whose consumer graph is being launched
     std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
     std::array<std::array<DevBuf, 16>, 2> scratch_bufs_;
 

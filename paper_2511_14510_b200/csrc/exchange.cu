@@ -22,30 +22,30 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 // Waits until every layer's counter holds this step's arrivals from all peers
 // (B * H_local * (world - 1) per step; counters are monotonic, compared
-// wrap-safe), then copies the peers' rows of the step's slot into out.
-__global__ void __launch_bounds__(256) exchange_finish_kernel(EngineView v) {
-    __shared__ int s_ok;
+// wrap-safe). One warp: a spinning kernel must not hold SM slots that a peer
+// sharing the device (tests, MPS) needs for its own attention.
+__global__ void exchange_wait_kernel(EngineView v) {
+    if (threadIdx.x != 0) return;
     const int t = *v.dev_step + 1;
     const unsigned target = (unsigned)t * (unsigned)(v.B * v.H * (v.world - 1));
-    if (threadIdx.x == 0) {
-        const unsigned* flags = v.xflag[v.rank];
-        const uint64_t t0 = global_ns();
-        int ok = 1;
-        for (int l = 0; l < v.L && ok; ++l) {
-            while ((int)(ld_acquire_sys(flags + l) - target) < 0) {
-                if (global_ns() - t0 > v.xtimeout_ns) {
-                    raise_err(v.err, kErrExchange);
-                    ok = 0;
-                    break;
-                }
-                __nanosleep(100);
+    const unsigned* flags = v.xflag[v.rank];
+    const uint64_t t0 = global_ns();
+    for (int l = 0; l < v.L; ++l) {
+        while ((int)(ld_acquire_sys(flags + l) - target) < 0) {
+            if (global_ns() - t0 > v.xtimeout_ns) {
+                raise_err(v.err, kErrExchange);
+                return;
             }
+            __nanosleep(100);
         }
-        s_ok = ok;
     }
-    __syncthreads();
-    if (!s_ok) return;
-    // peers' head blocks: rows (b, l, q) with q outside [q0, q0 + HQ)
+}
+
+// Then the peers' head blocks (rows (b, l, q), q outside [q0, q0 + HQ)) of
+// this step's slot -> out. Ordered after the wait by the stream; a timed-out
+// wait leaves out's peer blocks as they were (the error flag reports it).
+__global__ void __launch_bounds__(256) exchange_copy_kernel(EngineView v) {
+    const int t = *v.dev_step + 1;
     const float* slot = v.xslot[v.rank];
     float* out = v.desc->out;
     const int vec = v.d / 4;  // d is a multiple of 8
@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(256) exchange_finish_kernel(EngineView v) {
 void launch_exchange_finish(const EngineView& v, cudaStream_t stream) {
     const size_t vecs = (size_t)v.B * v.L * (v.HQg - v.HQ) * (v.d / 4);
     const int grid = (int)std::min<size_t>((vecs + 255) / 256, (size_t)kNumSMs);
-    exchange_finish_kernel<<<grid < 1 ? 1 : grid, 256, 0, stream>>>(v);
+    exchange_wait_kernel<<<1, 32, 0, stream>>>(v);
+    exchange_copy_kernel<<<grid < 1 ? 1 : grid, 256, 0, stream>>>(v);
 }
 
 }  // namespace clo

@@ -4,6 +4,12 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# Several engines share ONE device in the exchange tests (each with 3-4 CUDA
+# streams, plus the caller's). With the default 8 hardware work queues their
+# streams alias, and a peer-waiting kernel would then block the very peer it
+# waits for. One engine per GPU (production) never shares a queue.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
