@@ -203,7 +203,7 @@ void Engine::allocate() {
     d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
     d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k + 64);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
-        d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_, false);
+        d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_ + 64, false);
         // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
         // (engine.cpp:172-174); stored transposed [d][bits] for coalesced reads.
         std::vector<double> pt((size_t)L * H * d * cfg_.hash_bits);

@@ -2,6 +2,9 @@
 // See select.cuh for the semantics and the reference functions restated.
 #include <cub/block/block_scan.cuh>
 
+#include <cstdlib>
+#include <string>
+
 #include "select.cuh"
 
 namespace clo {
@@ -74,6 +77,128 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_kernel(SelArgs a
             out[b] = s;
         }
         __syncthreads();
+    }
+}
+
+// Same scoring with the codes streamed by the TMA engine: each 4096-row chunk
+// is four 1024-row pieces, bulk-copied (cp.async.bulk, one instruction per
+// piece from thread 0) into a 2-stage shared-memory ring while the CTA scores
+// the previous piece, so every CTA keeps a whole piece (32 KiB at 256 bits) in
+// flight instead of a few loads per thread. Rows of a partial last piece that
+// fall past its last whole 16 bytes are read from global directly.
+constexpr int kPieceRows = 1024;
+constexpr int kPieces = kScoreChunk / kPieceRows;  // 4
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int W>
+__global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelArgs a, int agg) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* stage = reinterpret_cast<uint64_t*>(sm);                              // [2][kPieceRows*W]
+    uint32_t* whist = reinterpret_cast<uint32_t*>(sm + 2 * kPieceRows * W * 8);     // [kWarps][nb]
+    uint64_t* qb = reinterpret_cast<uint64_t*>(sm + 2 * kPieceRows * W * 8 +
+                                               ((size_t)kWarps * a.nb * 4 + 7) / 8 * 8);  // [m][W]
+    __shared__ __align__(8) uint64_t bar[2];
+    const int units = *a.count * a.max_chunks;
+    const int mine = units > (int)blockIdx.x ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = mine * kPieces;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // rows [row0, row0 + rows) of piece i; rows = 0 for pieces past the item's end
+    auto piece = [&](int i, int& item, int& chunk, int& row0, int& rows) {
+        const int u = blockIdx.x + (i / kPieces) * gridDim.x;
+        item = u / a.max_chunks;
+        chunk = u % a.max_chunks;
+        row0 = chunk * kScoreChunk + (i % kPieces) * kPieceRows;
+        rows = max(0, min(kPieceRows, a.items[item].n - row0));
+    };
+    auto issue = [&](int i) {  // thread 0
+        int item, chunk, row0, rows;
+        piece(i, item, chunk, row0, rows);
+        const uint32_t bytes = (uint32_t)rows * W * 8 / 16 * 16;
+        uint64_t* b = &bar[i & 1];
+        if (bytes) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(stage + (size_t)(i & 1) * kPieceRows * W)),
+                "l"(a.items[item].codes + (size_t)row0 * W), "r"(bytes), "r"(smem_addr(b))
+                : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+        }
+    };
+    if (threadIdx.x == 0 && total > 0) issue(0);
+    for (int i = 0; i < total; ++i) {
+        int item, chunk, row0, rows;
+        piece(i, item, chunk, row0, rows);
+        const int p = i % kPieces;
+        if (p == 0) {  // a new chunk: its histogram and the item's query bits
+            for (int x = threadIdx.x; x < kWarps * a.nb; x += blockDim.x) whist[x] = 0;
+            for (int x = threadIdx.x; x < a.m * W; x += blockDim.x) {
+                const int j = x / W, w = x % W;
+                qb[x] = a.qbits[((size_t)item * a.m + j) * a.words + w];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0 && i + 1 < total) issue(i + 1);
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_addr(&bar[i & 1])),
+            "r"((i >> 1) & 1)
+            : "memory");
+        const uint64_t* st = stage + (size_t)(i & 1) * kPieceRows * W;
+        const int copied = rows * W * 8 / 16 * 16 / (W * 8);  // whole rows in smem
+        const uint64_t* codes = a.items[item].codes;
+        uint16_t* keys = a.key16 + (size_t)item * a.nmax;
+        uint32_t* myhist = whist + warp * a.nb;
+#pragma unroll 4
+        for (int r = threadIdx.x; r < rows; r += kScoreThreads) {
+            uint64_t c[W];
+            if (r < copied) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) c[w] = st[(size_t)r * W + w];
+            } else {
+#pragma unroll
+                for (int w = 0; w < W; ++w) c[w] = __ldg(codes + (size_t)(row0 + r) * W + w);
+            }
+            int best = 0;
+            for (int j = 0; j < a.m; ++j) {
+                int dist = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qb[j * W + w]);
+                best = max(best, a.bits - dist);
+            }
+            keys[row0 + r] = static_cast<uint16_t>(best);
+            if (agg) {  // warp-aggregated: one shared atomic per distinct score
+                const unsigned act = __activemask();
+                const unsigned same = __match_any_sync(act, best);
+                if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&myhist[best], (uint32_t)__popc(same));
+            } else {
+                atomicAdd(&myhist[best], 1u);
+            }
+        }
+        __syncthreads();  // stage i & 1 is free; the chunk's histogram is complete after its last piece
+        if (p == kPieces - 1) {
+            uint32_t* out = a.chunk_hist + ((size_t)item * a.max_chunks + chunk) * a.nb;
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
+                uint32_t sum = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) sum += whist[w * a.nb + b];
+                out[b] = sum;
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -436,10 +561,35 @@ __global__ void chunk_prefix_kernel(SelArgs a) {
 
 void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
     const size_t sm_score = (size_t)kWarps * a.nb * 4 + 8 + (size_t)a.m * a.words * 8;
+    static const bool tma = [] {  // CLO_SCORE=lsu: the register-load kernel
+        const char* e = getenv("CLO_SCORE");
+        return !(e && std::string(e) == "lsu");
+    }();
+    const size_t sm_tma = 2 * (size_t)kPieceRows * a.words * 8 + ((size_t)kWarps * a.nb * 4 + 7) / 8 * 8 +
+                          (size_t)a.m * a.words * 8;
+    static const int grid_cap = [] {  // CLO_SCORE_GRID: experiment switch
+        const char* e = getenv("CLO_SCORE_GRID");
+        return e && atoi(e) > 0 ? atoi(e) : 8 * kNumSMs;  // measured: more CTAs than resident slots balance the chunks
+    }();
+    const int grid_tma = a.grid < grid_cap ? a.grid : grid_cap;
+    static const int hist_agg = [] {  // CLO_SCORE_AGG=1: warp-aggregated histogram atomics
+        const char* e = getenv("CLO_SCORE_AGG");
+        return e && atoi(e) == 1 ? 1 : 0;
+    }();
     switch (a.words) {
-#define CLO_W(W)                                                                        \
-    case W:                                                                             \
-        score_signhash_kernel<W><<<a.grid, kScoreThreads, sm_score, stream>>>(a);       \
+#define CLO_W(W)                                                                                            \
+    case W:                                                                                                 \
+        if (tma) {                                                                                          \
+            static bool cfg = false;                                                                        \
+            if (!cfg) {                                                                                     \
+                cudaFuncSetAttribute(score_signhash_tma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)(2 * kPieceRows * W * 8 + 8 * 520 * 4 + 16 * 8 * 8));             \
+                cfg = true;                                                                                 \
+            }                                                                                               \
+            score_signhash_tma_kernel<W><<<grid_tma, kScoreThreads, sm_tma, stream>>>(a, hist_agg);           \
+        } else {                                                                                            \
+            score_signhash_kernel<W><<<a.grid, kScoreThreads, sm_score, stream>>>(a);                       \
+        }                                                                                                   \
         break;
         CLO_W(1) CLO_W(2) CLO_W(3) CLO_W(4) CLO_W(5) CLO_W(6) CLO_W(7) CLO_W(8)
 #undef CLO_W
