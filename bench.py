@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--huge", action="store_true",
+                    help="back the pinned host KV store with 2 MiB pages (GPU TLB reach for large stores)")
     ap.add_argument("--same-device", action="store_true",
                     help="testing only: every rank on cuda:0 with a gloo group (multi-rank functional check)")
     ap.add_argument("--allgather", default="fused", choices=["fused", "nccl"],
@@ -295,7 +297,7 @@ def run_ours(args):
     t_setup = time.time()
 
     # host KV: one aliased [B][1][H][nmax][d] bf16 buffer pair (see module doc)
-    hkv = HostKV(B, 1, H, nmax, d, "bf16")
+    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge)
     for b in range(B):
         for arr in (hkv.k, hkv.v):
             x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)

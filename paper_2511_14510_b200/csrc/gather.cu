@@ -16,6 +16,9 @@
 //              in flight per CTA) and store them into their slots.
 #include <cub/block/block_scan.cuh>
 
+#include <cstdlib>
+#include <string>
+
 #include "gather.cuh"
 
 namespace clo {
@@ -350,6 +353,102 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const char* __restrict__
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Engine gather on the TMA engine (CLO_GATHER=tma): each warp streams groups
+// of 32 fetch-list rows — lane r bulk-copies row r (one cp.async.bulk of a
+// whole row) from pinned host memory into a shared-memory stage, completion on
+// an mbarrier, then bulk-stores it to its HBM slot. kTmaStages groups per warp
+// in flight. Groups are (missed head, matrix, 32-row block) of the layer.
+constexpr int kTmaWarps = 4;
+
+__global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(GatherEngineArgs a) {
+    extern __shared__ __align__(128) char tstage[];  // [warp][kTmaStages][32][row_bytes]
+    __shared__ __align__(8) uint64_t tbar[kTmaWarps][kTmaStages];
+    const EngineView& v = a.v;
+    const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gpm = (v.k + kTmaRows - 1) / kTmaRows;  // 32-row groups per matrix
+    const int total = a.count[a.layer] * 2 * gpm;
+    const int gw = blockIdx.x * kTmaWarps + warp, nw = gridDim.x * kTmaWarps;
+    const int mine = total > gw ? (total - 1 - gw) / nw + 1 : 0;
+    char* st0 = tstage + (size_t)warp * kTmaStages * kTmaRows * row_bytes;
+    if (lane == 0) {
+        for (int s = 0; s < kTmaStages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[warp][s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // group i of this warp -> (rows, host source of lane's row, slot destination)
+    auto locate = [&](int i, int& rows, const char*& src, char*& dst) {
+        const int gidx = gw + i * nw;
+        const int item = gidx / (2 * gpm), rem = gidx % (2 * gpm), mat = rem / gpm, grp = rem % gpm;
+        const size_t li = (size_t)a.layer * a.items_cap + item;
+        const int nf = a.fetch_count[li];
+        rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
+        src = nullptr;
+        dst = nullptr;
+        if (lane < rows) {
+            const int seg = a.items[li].seg;
+            const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+            const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+            const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+            const int r = grp * kTmaRows + lane;
+            src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.d) * dtype_size(v.kv_dtype);
+            dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
+        }
+    };
+    auto load = [&](int i) {
+        int rows;
+        const char* src;
+        char* dst;
+        locate(i, rows, src, dst);
+        const int s = i % kTmaStages;
+        uint64_t* bar = &tbar[warp][s];
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (rows)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                             "r"(rows * row_bytes)
+                             : "memory");
+            else
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+        }
+        __syncwarp();
+        if (lane < rows)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(st0 + ((size_t)s * kTmaRows + lane) * row_bytes)),
+                "l"(src), "r"(row_bytes), "r"(smem_u32(bar))
+                : "memory");
+    };
+    for (int i = 0; i < min(kTmaStages, mine); ++i) load(i);
+    unsigned long long moved = 0;
+    for (int i = 0; i < mine; ++i) {
+        const int s = i % kTmaStages;
+        int rows;
+        const char* src;
+        char* dst;
+        locate(i, rows, src, dst);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra W_%=;\n\t}" ::"r"(smem_u32(&tbar[warp][s])),
+            "r"((i / kTmaStages) & 1)
+            : "memory");
+        if (lane < rows) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"(smem_u32(st0 + ((size_t)s * kTmaRows + lane) * row_bytes)), "r"(row_bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage reusable
+        }
+        moved += (unsigned long long)rows * row_bytes;
+        __syncwarp();
+        if (i + kTmaStages < mine) load(i + kTmaStages);
+    }
+    if (lane < 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (a.count_bytes && lane == 0 && moved) atomicAdd(v.gathered_bytes, moved);
+}
+
 }  // namespace
 
 void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int row_bytes, int k,
@@ -375,6 +474,21 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 }
 
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream) {
+    static const bool tma = [] {
+        const char* e = getenv("CLO_GATHER");
+        return e && std::string(e) == "tma";
+    }();
+    const int row_bytes = a.v.d * dtype_size(a.v.kv_dtype);
+    const size_t sm = (size_t)kTmaWarps * kTmaStages * kTmaRows * row_bytes;
+    if (tma && sm <= 200 * 1024) {  // rows up to 400 B: the ring fits one CTA per SM
+        static size_t configured = 0;
+        if (sm > 48 * 1024 && sm > configured) {
+            cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            configured = sm;
+        }
+        gather_engine_tma_kernel<<<grid, kTmaWarps * 32, sm, stream>>>(a);
+        return;
+    }
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 

@@ -134,7 +134,7 @@ def profiles_from_arrays(tau: np.ndarray, q_importance: np.ndarray):
 class HostKV:
     """Pinned, UVA-mapped host K/V store [B][Lk][H][nmax][d] (HeadStore::k/v)."""
 
-    def __init__(self, batch, layers, heads, nmax, d, kv_dtype):
+    def __init__(self, batch, layers, heads, nmax, d, kv_dtype, hugepages: bool = False):
         lib = _lib.load()
         self.np_dtype = np.uint16 if kv_dtype == "bf16" else np.float32
         self.shape = (batch, layers, heads, nmax, d)
@@ -143,7 +143,7 @@ class HostKV:
         arrays = []
         for _ in range(2):
             p = C.c_void_p()
-            check(lib.clo_host_alloc(nbytes, C.byref(p)))
+            check(lib.clo_host_alloc_ex(nbytes, _lib.HOST_HUGEPAGES if hugepages else 0, C.byref(p)))
             self._ptrs.append(p.value)
             buf = (C.c_char * nbytes).from_address(p.value)
             arrays.append(np.frombuffer(buf, dtype=self.np_dtype).reshape(self.shape))
