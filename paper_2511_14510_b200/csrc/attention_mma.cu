@@ -110,6 +110,7 @@ struct MmaPlan {
     int G;       // CTAs
     int R;       // partial runs per warp
     int W;       // warps per CTA (each warp flushes its own partials)
+    int single;  // G == B*H: CTA j serves exactly head j (warp partials merge in shared memory)
     int seg[kMaxCtas + 1];  // segment starts S_j = j*T/G (T < 2^31)
 };
 
@@ -265,16 +266,25 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
                                                                        float* part) {
     using T = __nv_bfloat16;
     constexpr uint32_t kRowBytes = D * 2;
-    constexpr uint32_t kPitch = kRowBytes + 16;           // padded smem row (bank-conflict free ldmatrix)
-    constexpr uint32_t kStageBytes = 2 * kTileM * kPitch; // K rows then V rows
+    constexpr uint32_t kMatBytes = kTileM * kRowBytes;    // one matrix tile, 128B-swizzled
+    constexpr uint32_t kStageBytes = 2 * kMatBytes;       // K tile then V tile
     constexpr int KS = D / 16;                            // k-steps of QK
     constexpr int NT = D / 8;                             // dim tiles of PV
     constexpr int CPR = kRowBytes / 16;                   // 16-byte chunks per row
     constexpr int RPR = 32 / CPR;                         // rows per warp-wide copy round
     static_assert(M >= 1 && M <= 8, "m <= 8");
 
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ __align__(16) int32_t toks[kWarpsM][kStagesM][kTileM];
+    __shared__ __align__(8) uint64_t full[kWarpsM][kStagesM];
+    // Stage layout = the TMA 128-byte swizzle: a matrix tile is D/64 column
+    // halves of [kTileM rows][128 B]; 16-byte chunk cc of row r of a half sits
+    // at r*128 + ((cc ^ (r & 7)) * 16). ldmatrix over 8 rows then hits 8
+    // distinct bank groups, and contiguous slot tiles arrive as one 2D TMA box
+    // per half.
+    auto swz = [](int r, int c) -> uint32_t {  // row r, 16-byte chunk c of a matrix tile
+        return (uint32_t)((c >> 3) * (kTileM * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    };
 
     const int j = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,13 +338,25 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
             if (lane < sel_rows)
                 cp_async4(smem_u32(&toks[warp][s][lane]), (pers ? idx : v.slot_tok + oslot * v.k) + tp + lane);
             const int ch = lane % CPR, r0 = lane / CPR;
-            if (!pers && tp + kTileM <= v.k) {  // a run of contiguous cache slots
-                const T* kr = static_cast<const T*>(v.slot_k) + (oslot * v.k + tp) * D + ch * 8;
-                const T* vr = static_cast<const T*>(v.slot_v) + (oslot * v.k + tp) * D + ch * 8;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our ldmatrix reads of the stage
+            __syncwarp();
+            if (!pers && tp + kTileM <= v.k && v.tmap_k) {
+                // a run of contiguous cache slots: one 2D TMA box per matrix half
+                if (lane == 0) {
+                    uint64_t* bar = &full[warp][s];
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                                 "r"(kStageBytes)
+                                 : "memory");
+                    const int row0 = (int)(oslot * v.k + tp);
 #pragma unroll
-                for (int rr = r0; rr < kTileM; rr += RPR) {
-                    cp_async16(st + rr * kPitch + ch * 16, kr + (size_t)rr * D);
-                    cp_async16(st + (kTileM + rr) * kPitch + ch * 16, vr + (size_t)rr * D);
+                    for (int m2 = 0; m2 < 2; ++m2)
+#pragma unroll
+                        for (int hh = 0; hh < D / 64; ++hh)
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%2, %3}], [%4];" ::"r"(st + m2 * kMatBytes + hh * kTileM * 128),
+                                "l"(m2 ? v.tmap_v : v.tmap_k), "r"(hh * 64), "r"(row0), "r"(smem_u32(bar))
+                                : "memory");
                 }
             } else {
                 const size_t pslot = pers ? (size_t)b * v.NP + v.pidx[lg] : 0;
@@ -369,9 +391,11 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
                             vr = wv + (size_t)wr * D;
                         }
                     }
-                    cp_async16(st + rr * kPitch + ch * 16, kr + ch * 8);
-                    cp_async16(st + (kTileM + rr) * kPitch + ch * 16, vr + ch * 8);
+                    cp_async16(st + swz(rr, ch), kr + ch * 8);
+                    cp_async16(st + kMatBytes + swz(rr, ch), vr + ch * 8);
                 }
+                if (lane == 0)  // data readiness of LDGSTS stages: the commit group below
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[warp][s])) : "memory");
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -381,6 +405,10 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
     // finite stale values (weight 0), never uninitialised NaN patterns
     for (uint32_t i = lane; i < kStagesM * kStageBytes / 16; i += 32)
         reinterpret_cast<uint4*>(ring)[i] = make_uint4(0, 0, 0, 0);
+    if (lane == 0)
+        for (int s2 = 0; s2 < kStagesM; ++s2)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[warp][s2])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     for (int i = 0; i < kStagesM - 1; ++i) issue(i);
 
@@ -467,7 +495,7 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
             ++chd;
         }
         if (h != cur) {
-            if (cur >= 0) flush();
+            if (cur >= 0) flush();  // never in single mode: a CTA's tiles are one head
             load_q(h);
             cur = h;
             run_tiles = 0;
@@ -476,10 +504,16 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         ++run_tiles;
         const int rows = min(kTileM, P - tp);
         const int s = i % kStagesM;
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStagesM - 1) : "memory");  // tile i landed
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStagesM - 1) : "memory");  // LDGSTS part of tile i
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(&full[warp][s])),
+            "r"((i / kStagesM) & 1)
+            : "memory");  // TMA part of tile i
         __syncwarp();
         const uint32_t kbase = smem_u32(ring + (size_t)s * kStageBytes);
-        const uint32_t vbase = kbase + kTileM * kPitch;
+        const uint32_t vbase = kbase + kMatBytes;
 
         // ---- S = Q K^T for TM keys: NK key tiles of 8, two independent
         // accumulator chains per key tile (even / odd k-steps) ---------------
@@ -492,7 +526,7 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
 #pragma unroll
             for (int kp = 0; kp < KS / 2; ++kp) {
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(kbase + (nt * 8 + (lane & 7)) * kPitch + (kp * 32 + (lane >> 3) * 8) * 2, b0, b1, b2, b3);
+                ldsm_x4(kbase + swz(nt * 8 + (lane & 7), kp * 4 + (lane >> 3)), b0, b1, b2, b3);
                 mma16816(sacc[nt][0], qa[2 * kp], b0, b1);
                 mma16816(sacc[nt][1], qa[2 * kp + 1], b2, b3);
             }
@@ -548,8 +582,8 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
 #pragma unroll
             for (int nd = 0; nd < NT / 2; ++nd) {
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vbase + (kt * 16 + (lane >> 3 & 1) * 8 + (lane & 7)) * kPitch + (nd * 16 + (lane >> 4) * 8) * 2,
-                          b0, b1, b2, b3);
+                ldsm_x4_t(vbase + swz(kt * 16 + (lane >> 3 & 1) * 8 + (lane & 7), nd * 2 + (lane >> 4)), b0, b1, b2,
+                          b3);
                 mma16816(o[2 * nd], pa, b0, b1);
                 mma16816(o[2 * nd + 1], pa, b2, b3);
             }
@@ -557,7 +591,47 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         __syncwarp();  // stage s is free for the issue S-1 tiles on
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (cur >= 0) flush();
+    if (!pl.single) {
+        if (cur >= 0) flush();
+        return;
+    }
+    // One head per CTA: the warps' (m, l, O) merge through shared memory by
+    // the whole CTA (fixed warp order: deterministic), no global partials.
+    __syncthreads();  // every warp is done with its ring
+    float* red = reinterpret_cast<float*>(smem);  // [kWarpsM][M][D + 2]
+    {
+        float lsum = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+        if (qg < M) {
+            float* rw = red + ((size_t)warp * M + qg) * (D + 2);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                rw[nt * 8 + 2 * qc] = o[nt][0] + o[nt][2];
+                rw[nt * 8 + 2 * qc + 1] = o[nt][1] + o[nt][3];
+            }
+            if (qc == 0) {
+                rw[D] = m_run;
+                rw[D + 1] = lsum;
+            }
+        }
+    }
+    __syncthreads();
+    const int h = j, hb = h / v.H, g = h - hb * v.H;
+    for (int x = threadIdx.x; x < M * D; x += kWarpsM * 32) {
+        const int q = x / D, e = x - q * D;
+        float gm = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < kWarpsM; ++w) gm = fmaxf(gm, red[((size_t)w * M + q) * (D + 2) + D]);
+        float a = 0.f, den = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarpsM; ++w) {
+            const float cw = wexp(red[((size_t)w * M + q) * (D + 2) + D], gm);
+            a += red[((size_t)w * M + q) * (D + 2) + e] * cw;
+            den += red[((size_t)w * M + q) * (D + 2) + D + 1] * cw;
+        }
+        emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+    }
+    signal_head_output(v, l);
 }
 
 MmaPlan make_plan(const EngineView& v, int W, int ctas_per_sm, int TM) {
@@ -579,6 +653,7 @@ MmaPlan make_plan(const EngineView& v, int W, int ctas_per_sm, int TM) {
     const long long most = (pl.T + W - 1) / W;  // at least a tile per warp
     if (G > most) G = most;
     pl.G = (int)G;
+    pl.single = G == BH;
     for (int j = 0; j <= pl.G; ++j) pl.seg[j] = (int)((long long)j * pl.T / pl.G);
     const long long seg = (pl.T + pl.G - 1) / pl.G;
     pl.R = (int)((seg + pl.N - 1) / pl.N) + 1;
@@ -606,7 +681,7 @@ MmaShape mma_shape() {
 template <int D, int M, int W, int S, int C, int TM, int RC>
 void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
     const MmaPlan pl = make_plan(v, W, C, TM);
-    const size_t ring = (size_t)W * S * 2 * TM * (D * 2 + 16);
+    const size_t ring = (size_t)W * S * 2 * TM * D * 2;
     const size_t sm = ring + (size_t)pl.R * M * D * sizeof(float);  // + staged queries
     static size_t configured = 0;
     if (sm > configured) {
@@ -614,7 +689,12 @@ void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         configured = sm;
     }
-    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(v, layer, pl, v.attn_part);
+    EngineView vv = v;
+    if (TM == 32) {  // the tensor maps whose boxes match the tile
+        vv.tmap_k = v.tmap_k32;
+        vv.tmap_v = v.tmap_v32;
+    }
+    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(vv, layer, pl, v.attn_part);
 }
 
 // Register cap: CLO_ATTN_REGCAP=184 lets an 8-warp CTA share its SM with a

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstring>
 #include <unistd.h>
+
+#include <cuda.h>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -254,6 +256,39 @@ void Engine::allocate() {
             CLO_CUDA(cudaMemcpy(d_off_layers_.p, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
     }
 
+    // TMA tensor maps over the cache slots for the tensor-core attention:
+    // [B*NO*k rows][d] bf16, boxes of 64 columns x 16 or 32 rows, 128-byte
+    // swizzle (the kernel's stage layout). cuTensorMapEncodeTiled comes from
+    // the driver through the runtime's entry-point query (no -lcuda).
+    if (cfg_.kv_dtype == CLO_DTYPE_BF16 && (d == 64 || d == 128) && no_ > 0) {
+        using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
+            auto encode = reinterpret_cast<EncodeFn>(fn);
+            CUtensorMap maps[4];
+            bool ok = true;
+            const cuuint64_t rows = (cuuint64_t)B * no_ * k;
+            for (int i = 0; i < 4; ++i) {
+                const cuuint64_t dims[2] = {(cuuint64_t)d, rows};
+                const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+                const cuuint32_t box[2] = {64, i < 2 ? 16u : 32u};
+                const cuuint32_t estr[2] = {1, 1};
+                ok = ok && encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (i & 1) ? d_slot_v_.p : d_slot_k_.p,
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            if (ok) {
+                d_tmaps_.alloc(sizeof(maps));
+                CLO_CUDA(cudaMemcpy(d_tmaps_.p, maps, sizeof(maps), cudaMemcpyHostToDevice));
+            }
+        }
+        cudaGetLastError();
+    }
+
     // staging for host-resident step inputs / outputs
     d_in_tq_.alloc(sizeof(float) * B * L * HQ * d, false);
     d_in_aq_.alloc(sizeof(float) * B * L * HQ * d, false);
@@ -418,6 +453,13 @@ EngineView Engine::view() const {
     v.world = world_;
     v.rank = rank_;
     v.xtimeout_ns = exchange_timeout_ns();
+    if (d_tmaps_.p) {
+        const char* tm = d_tmaps_.as<char>();
+        v.tmap_k = tm;
+        v.tmap_v = tm + sizeof(CUtensorMap);
+        v.tmap_k32 = tm + 2 * sizeof(CUtensorMap);
+        v.tmap_v32 = tm + 3 * sizeof(CUtensorMap);
+    }
     v.HQg = world_ * s.num_q_heads;
     v.q0 = rank_ * s.num_q_heads;
     for (int r = 0; r < world_; ++r) {

@@ -97,6 +97,7 @@ class Engine {
     DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_, d_xfer_, d_off_layers_;
     int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
+    DevBuf d_tmaps_;  // 4 CUtensorMaps over the cache slots (attention TMA boxes)
     // host-input staging, double-buffered: step t+1's H2D copies run on a copy
     // stream while step t's graph still executes
     std::array<DevBuf, 2> d_in_;

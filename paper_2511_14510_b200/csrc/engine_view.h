@@ -126,6 +126,13 @@ struct EngineView {
     float* xslot[kMaxRanks];     // rank r's exchange slots [2][B][L][HQg][d]
     unsigned* xflag[kMaxRanks];  // rank r's per-layer arrival counters [L]
     unsigned long long xtimeout_ns;  // a peer silent this long is reported lost
+    // TMA tensor maps (CUtensorMap, 64-byte aligned, device memory) over the
+    // cache slots [B*NO*k][d] bf16: 128-byte swizzled boxes of 64 columns x
+    // the attention tile rows; null when not built (f32 rows, other d)
+    const void* tmap_k;    // 16-row boxes
+    const void* tmap_v;
+    const void* tmap_k32;  // 32-row boxes
+    const void* tmap_v32;
 };
 
 }  // namespace clo
