@@ -110,7 +110,8 @@ struct MmaPlan {
     int G;       // CTAs
     int R;       // partial runs per warp
     int W;       // warps per CTA (each warp flushes its own partials)
-    int single;  // G == B*H: CTA j serves exactly head j (warp partials merge in shared memory)
+    int single;  // G = c * B*H: CTA j serves piece j % c of head j / c (warps merge in shared memory)
+    int c;       // CTAs per head when single
     int seg[kMaxCtas + 1];  // segment starts S_j = j*T/G (T < 2^31)
 };
 
@@ -595,8 +596,10 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         if (cur >= 0) flush();
         return;
     }
-    // One head per CTA: the warps' (m, l, O) merge through shared memory by
-    // the whole CTA (fixed warp order: deterministic), no global partials.
+    // Head-aligned segments: the warps' (m, l, O) merge through shared memory
+    // by the whole CTA (fixed warp order: deterministic). With c > 1 CTAs per
+    // head, each CTA then writes one partial (m, l, unnormalised O) and the
+    // last of the head's c CTAs merges them in piece order.
     __syncthreads();  // every warp is done with its ring
     float* red = reinterpret_cast<float*>(smem);  // [kWarpsM][M][D + 2]
     {
@@ -616,7 +619,8 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         }
     }
     __syncthreads();
-    const int h = j, hb = h / v.H, g = h - hb * v.H;
+    const int h = j / pl.c, piece = j - h * pl.c, hb = h / v.H, g = h - hb * v.H;
+    float* ph = part + (size_t)h * pl.c * M * (D + 4);  // [c][M][D + 4] partials of head h
     for (int x = threadIdx.x; x < M * D; x += kWarpsM * 32) {
         const int q = x / D, e = x - q * D;
         float gm = -CUDART_INF_F;
@@ -629,7 +633,39 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
             a += red[((size_t)w * M + q) * (D + 2) + e] * cw;
             den += red[((size_t)w * M + q) * (D + 2) + D + 1] * cw;
         }
-        emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+        if (pl.c == 1) {
+            emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+        } else {
+            float* pp = ph + ((size_t)piece * M + q) * (D + 4);
+            __stcg(pp + e, a);
+            if (e == 0) {
+                __stcg(pp + D, gm);
+                __stcg(pp + D + 1, den);
+            }
+        }
+    }
+    if (pl.c > 1) {
+        __shared__ int s_last_cta;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last_cta = atomicAdd(&v.attn_count[h], 1) == pl.c - 1;
+        __syncthreads();
+        if (!s_last_cta) return;
+        __threadfence();
+        for (int x = threadIdx.x; x < M * D; x += kWarpsM * 32) {
+            const int q = x / D, e = x - q * D;
+            float gm = -CUDART_INF_F;
+            for (int cc = 0; cc < pl.c; ++cc) gm = fmaxf(gm, __ldcg(ph + ((size_t)cc * M + q) * (D + 4) + D));
+            float a = 0.f, den = 0.f;
+            for (int cc = 0; cc < pl.c; ++cc) {
+                const float* pp = ph + ((size_t)cc * M + q) * (D + 4);
+                const float cw = wexp(__ldcg(pp + D), gm);
+                a += __ldcg(pp + e) * cw;
+                den += __ldcg(pp + D + 1) * cw;
+            }
+            emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+        }
+        if (threadIdx.x == 0) v.attn_count[h] = 0;
     }
     signal_head_output(v, l);
 }
@@ -653,7 +689,8 @@ MmaPlan make_plan(const EngineView& v, int W, int ctas_per_sm, int TM) {
     const long long most = (pl.T + W - 1) / W;  // at least a tile per warp
     if (G > most) G = most;
     pl.G = (int)G;
-    pl.single = G == BH;
+    pl.single = G % BH == 0;
+    pl.c = pl.single ? (int)(G / BH) : 0;
     for (int j = 0; j <= pl.G; ++j) pl.seg[j] = (int)((long long)j * pl.T / pl.G);
     const long long seg = (pl.T + pl.G - 1) / pl.G;
     pl.R = (int)((seg + pl.N - 1) / pl.N) + 1;
@@ -763,7 +800,8 @@ size_t attention_mma_partial_floats(int B, int H, int m, int d, int k, int sink,
     v.sink = sink;
     v.recent = recent;
     const int N = (k + sink + recent + kTileMin - 1) / kTileMin;
-    return (size_t)B * H * N * m * (d + 4);  // partial slots [B*H][N tiles], rows padded to 16 B
+    const int slots = N > 2 * kNumSMs ? N : 2 * kNumSMs;  // per head: tile runs, or CTA pieces (c <= G)
+    return (size_t)B * H * slots * m * (d + 4);  // partials, rows padded to 16 B
 }
 
 bool launch_attention_mma(const EngineView& v, int layer, cudaStream_t stream) {
