@@ -131,6 +131,14 @@ struct PartitionPlan {
 // ---- DecodeEngine (engine.hpp:91-139) -------------------------------------
 // The StepSource is replaced by explicit per-step inputs (device or host
 // buffers), since the step data lives on the GPU.
+// PipelineTimeline (pipeline_sim.hpp:74-86), measured on the device.
+struct PipelineTimeline {
+    std::vector<clo_layer_timing> per_layer;
+    clo_layer_timing totals{};
+    uint64_t steps = 0;
+    double share(double part_s) const { return totals.total_s > 0.0 ? part_s / totals.total_s : 0.0; }
+};
+
 class DecodeEngine {
   public:
     DecodeEngine(const EngineConfig& cfg, const HeadProfiles& profiles, const PartitionPlan& plan,
@@ -196,6 +204,34 @@ class DecodeEngine {
         s.resize(need ? need - 1 : 0);
         return s;
     }
+    // DecodeEngine::timeline() (engine.hpp:105): a decode step that also
+    // measures the per-layer LayerTiming breakdown, and the accumulated result.
+    void decode_step_timed(const clo_step_io& io, void* stream = nullptr) {
+        check(clo_engine_timeline_step(e_, &io, stream));
+    }
+    PipelineTimeline timeline() const {
+        PipelineTimeline tl;
+        tl.per_layer.resize(cfg_.shape.num_layers);
+        check(clo_get_timeline(e_, tl.per_layer.data(), (int)tl.per_layer.size(), &tl.totals, &tl.steps));
+        return tl;
+    }
+    std::string timeline_json() const {  // breakdown_to_json (pipeline_sim.cpp:115-135)
+        size_t need = 0;
+        check(clo_timeline_json(e_, nullptr, 0, &need));
+        std::string s(need, '\0');
+        check(clo_timeline_json(e_, s.data(), need, &need));
+        s.resize(need ? need - 1 : 0);
+        return s;
+    }
+    // KV-head sharding: the fused head-output all-gather (include/clo.h).
+    std::vector<char> exchange_handle(int rank, int world) {
+        std::vector<char> h(CLO_EXCHANGE_HANDLE_BYTES);
+        check(clo_engine_exchange_handle(e_, rank, world, h.data()));
+        return h;
+    }
+    void attach_peers(const std::vector<char>& handles_in_rank_order) {
+        check(clo_engine_attach_peers(e_, handles_in_rank_order.data()));
+    }
     clo_engine* handle() const { return e_; }
 
   private:
@@ -223,6 +259,58 @@ inline std::vector<int> sink_recent_indices(int n, int sink, int recent, bool* c
 }
 inline uint64_t cache_bytes(int offloaded, int entry_k, int held, int L, int hq, int d, int e) {
     return clo_cache_bytes(offloaded, entry_k, held, L, hq, d, e);
+}
+
+// ---- traces (trace_io.hpp:41-64) --------------------------------------------
+// TraceSource over libclo's reader; rows converted to the engine's storage type.
+class TraceSource {
+  public:
+    explicit TraceSource(const std::string& path) { check(clo_trace_open(path.c_str(), &t_)); }
+    ~TraceSource() { clo_trace_close(t_); }
+    TraceSource(const TraceSource&) = delete;
+    TraceSource& operator=(const TraceSource&) = delete;
+    ModelShape shape() const {
+        clo_model_shape s{};
+        check(clo_trace_info(t_, &s, nullptr, nullptr, nullptr));
+        return ModelShape{s.num_layers, s.num_q_heads, s.num_kv_heads, s.head_dim, s.bytes_per_element};
+    }
+    int prompt_tokens() const {
+        int n = 0;
+        check(clo_trace_info(t_, nullptr, &n, nullptr, nullptr));
+        return n;
+    }
+    int decode_steps() const {
+        int n = 0;
+        check(clo_trace_info(t_, nullptr, nullptr, &n, nullptr));
+        return n;
+    }
+    // prompt K/V rows of (layer, kv_head) as `dtype` (clo_dtype)
+    void prompt(int layer, int kv_head, int dtype, void* k_out, void* v_out) const {
+        check(clo_trace_prompt(t_, layer, kv_head, dtype, k_out, v_out));
+    }
+    // step t in the engine's clo_step_io layout (queries f32, rows `dtype`)
+    void step(int t, float* true_q, float* approx_q, void* new_k, void* new_v, int dtype) const {
+        check(clo_trace_step(t_, t, true_q, approx_q, new_k, new_v, dtype));
+    }
+    const clo_trace* handle() const { return t_; }
+
+  private:
+    clo_trace* t_ = nullptr;
+};
+
+// ---- profiling (profiler.hpp:12-36) -----------------------------------------
+inline std::vector<std::vector<clo_head_profile>> profile_heads(const std::vector<const TraceSource*>& sources,
+                                                                const clo_profiler_config& cfg,
+                                                                const double* provided_importance = nullptr) {
+    std::vector<const clo_trace*> h;
+    for (const TraceSource* s : sources) h.push_back(s->handle());
+    const ModelShape sh = sources.at(0)->shape();
+    std::vector<clo_head_profile> flat((size_t)sh.num_layers * sh.num_kv_heads);
+    check(clo_profile_heads(h.data(), (int)h.size(), &cfg, provided_importance, flat.data()));
+    std::vector<std::vector<clo_head_profile>> out(sh.num_layers);
+    for (int l = 0; l < sh.num_layers; ++l)
+        out[l].assign(flat.begin() + (size_t)l * sh.num_kv_heads, flat.begin() + (size_t)(l + 1) * sh.num_kv_heads);
+    return out;
 }
 
 }  // namespace clo::kvsim

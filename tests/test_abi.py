@@ -134,5 +134,9 @@ def test_cpp_shim_compiles_links_and_runs(tmp_path):
         gpu = torch.cuda.is_available()
     except ImportError:
         gpu = False
-    r = subprocess.run([str(exe)] + (["gpu"] if gpu else []), capture_output=True, text=True)
+    from paper_2511_14510_b200.trace import record_trace
+    from paper_2511_14510_b200.workload import Shape, SyntheticWorkload
+    trace = tmp_path / "t.bin"
+    record_trace(SyntheticWorkload(Shape(2, 4, 2, 8), batch=1, n_prompt=16, steps=2, kv_dtype="f32"), trace)
+    r = subprocess.run([str(exe), "gpu" if gpu else "cpu", str(trace)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
