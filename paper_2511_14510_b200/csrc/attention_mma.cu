@@ -720,12 +720,10 @@ void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
     const MmaPlan pl = make_plan(v, W, C, TM);
     const size_t ring = (size_t)W * S * 2 * TM * D * 2;
     const size_t sm = ring + (size_t)pl.R * M * D * sizeof(float);  // + staged queries
-    static size_t configured = 0;
-    if (sm > configured) {
-        cudaFuncSetAttribute(attn_mma_stream_kernel<D, M, W, S, C, TM, RC>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        configured = sm;
-    }
+    // per device (a process may drive several GPUs); launches happen at graph
+    // capture, so the host call is not on the replay path
+    cudaFuncSetAttribute(attn_mma_stream_kernel<D, M, W, S, C, TM, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     EngineView vv = v;
     if (TM == 32) {  // the tensor maps whose boxes match the tile
         vv.tmap_k = v.tmap_k32;

@@ -505,11 +505,7 @@ void launch_tma(const EngineView& v, int layer, dim3 grid, cudaStream_t stream) 
     const size_t tiles = (size_t)kStages * 2 * kTileRows * D * sizeof(T);
     const size_t red = (size_t)kWarps * M * (D + 2) * sizeof(float);
     const size_t sm = tiles > red ? tiles : red;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(attn_tma_kernel<T, D, M, LMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        configured = true;
-    }
+    cudaFuncSetAttribute(attn_tma_kernel<T, D, M, LMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attn_tma_kernel<T, D, M, LMAX><<<grid, kThreads, sm, stream>>>(v, layer);
 }
 

@@ -456,11 +456,7 @@ void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int ro
     const int groups = (k + kTmaRows - 1) / kTmaRows;
     const int grid = groups < ctas ? (groups > 0 ? groups : 1) : ctas;
     const size_t sm = (size_t)kTmaStages * kTmaRows * row_bytes;
-    static size_t configured = 0;
-    if (sm > 48 * 1024 && sm > configured) {
-        cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        configured = sm;
-    }
+    if (sm > 48 * 1024) cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     gather_tma_kernel<<<grid, 32, sm, stream>>>(static_cast<const char*>(src), static_cast<char*>(dst), idx,
                                                  row_bytes, k, n_rows, err);
 }
@@ -481,11 +477,8 @@ void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stre
     const int row_bytes = a.v.d * dtype_size(a.v.kv_dtype);
     const size_t sm = (size_t)kTmaWarps * kTmaStages * kTmaRows * row_bytes;
     if (tma && sm <= 200 * 1024) {  // rows up to 400 B: the ring fits one CTA per SM
-        static size_t configured = 0;
-        if (sm > 48 * 1024 && sm > configured) {
+        if (sm > 48 * 1024)
             cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            configured = sm;
-        }
         gather_engine_tma_kernel<<<grid, kTmaWarps * 32, sm, stream>>>(a);
         return;
     }

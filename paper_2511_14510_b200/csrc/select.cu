@@ -580,12 +580,8 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
 #define CLO_W(W)                                                                                            \
     case W:                                                                                                 \
         if (tma) {                                                                                          \
-            static bool cfg = false;                                                                        \
-            if (!cfg) {                                                                                     \
-                cudaFuncSetAttribute(score_signhash_tma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)(2 * kPieceRows * W * 8 + 8 * 520 * 4 + 16 * 8 * 8));             \
-                cfg = true;                                                                                 \
-            }                                                                                               \
+            cudaFuncSetAttribute(score_signhash_tma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                 (int)sm_tma);                                                              \
             score_signhash_tma_kernel<W><<<grid_tma, kScoreThreads, sm_tma, stream>>>(a, hist_agg);           \
         } else {                                                                                            \
             score_signhash_kernel<W><<<a.grid, kScoreThreads, sm_score, stream>>>(a);                       \
