@@ -62,19 +62,23 @@ void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, 
 // Sequential sign-hash dot products for a compile-time head dim: s_j +=
 // P^T[c][b] * q_j[c] for c = 0..D-1 in source order (separately rounded
 // multiply and add, bit-exact with the reference's scalar loop). Fully
-// unrolled, no bounds predicates, 16 P^T loads in flight per batch; the
+// unrolled, no bounds predicates, 32 P^T loads in flight per batch; the
 // products do not depend on the accumulators, so only the DADD chain is
 // serial.
+#ifndef CLO_HASH_BATCH
+#define CLO_HASH_BATCH 32
+#endif
 template <int D, int M>
 __device__ __forceinline__ void signhash_chain(const double* __restrict__ col, size_t stride, const double* q,
                                                int qstride, double (&s)[M]) {
+    constexpr int kB = CLO_HASH_BATCH;  // P^T loads in flight per thread
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 16) {
-        double p[16];
+    for (int c0 = 0; c0 < D; c0 += kB) {
+        double p[kB];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) p[i] = __ldg(col + (size_t)(c0 + i) * stride);
+        for (int i = 0; i < kB; ++i) p[i] = __ldg(col + (size_t)(c0 + i) * stride);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < kB; ++i)
 #pragma unroll
             for (int j = 0; j < M; ++j) s[j] = dmac(s[j], p[i], q[j * qstride + c0 + i]);
     }
