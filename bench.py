@@ -542,6 +542,29 @@ def run_ours(args):
                    "frac": sel_gbs / peaks["hbm_gbs"], "traffic": None, "share": sel_ms / total_prof,
                    "bytes_per_unit": "36 B per scored key (32 B code + u16 key write+read)"},
     }
+    # measured traffic / algorithmic bytes from the committed ncu captures,
+    # scaled to this run's per-launch algorithmic bytes (profiles/r1_traffic.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            tr = json.load(f)
+        launches_of = {"gather_zero_copy": per_kernel.get("gather_zero_copy", {}).get("launches", 1),
+                       "attention": attn_launches,
+                       "select": per_kernel.get("select_offloaded", {}).get("launches", 1)}
+        alg_per_launch = {"gather_zero_copy": prof_gathered / max(1, launches_of["gather_zero_copy"]),
+                          "attention": attn_bytes_launch,
+                          "select": sel_bytes / max(1, launches_of["select"])}
+        for kname, rl in rooflines.items():
+            t = tr.get(kname)
+            if not t:
+                continue
+            moved = t.get("pcie_read_bytes", 0) + t.get("dram_read_bytes", 0) + t.get("dram_write_bytes", 0) \
+                if kname != "gather_zero_copy" else t["pcie_read_bytes"]
+            ratio = moved / t["algorithmic_bytes"]
+            rl["traffic"] = ratio * alg_per_launch[kname]
+            rl["traffic_ratio"] = round(ratio, 4)
+            rl["traffic_source"] = "profiles/r1_traffic.json: " + t["capture"]
+    except (OSError, KeyError, ValueError):
+        pass
     dom_name = "gather_zero_copy" if dom == "gather_zero_copy" else (
         "attention" if dom == "attention" else ("select" if dom and dom.startswith("select") else dom))
     roof = dict(rooflines.get(dom_name, rooflines["attention"]))
