@@ -21,6 +21,10 @@
 
 #include "gather.cuh"
 
+#ifndef CLO_REC_THREADS
+#define CLO_REC_THREADS 1024
+#endif
+
 namespace clo {
 
 namespace {
@@ -30,7 +34,7 @@ constexpr int kUnroll = 4;
 constexpr int kVecsPerUnit = kGatherThreads * kUnroll;  // 16-byte vectors per work unit
 constexpr int kUnitUnroll = 8;                          // engine gather: loads in flight per thread
 constexpr int kUnitVecs = kGatherThreads * kUnitUnroll;  // 32 KiB of one matrix per unit
-constexpr int kRecThreads = 1024;
+constexpr int kRecThreads = CLO_REC_THREADS;
 
 __device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
     int lo = 0, hi = n;
