@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--huge", action="store_true", help="hugepage-backed pinned host store")
     ap.add_argument("--d", type=int, default=128, help="row width in bf16 elements (256 = K|V interleaved row)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--active", type=int, default=0,
+                    help="gather from only this many (random) heads of the store (0 = all)")
     args = ap.parse_args()
 
     import torch
@@ -78,10 +80,12 @@ def main():
     rng = np.random.default_rng(7)
     results = []
     for r in [int(x) for x in args.rows.split(",")]:
-        idx = np.concatenate([np.sort(rng.choice(n, r, replace=False)) + h * n for h in range(H)]).astype(np.int32)
+        heads = sorted(rng.choice(H, args.active, replace=False)) if args.active else range(H)
+        idx = np.concatenate([np.sort(rng.choice(n, r, replace=False)) + h * n for h in heads]).astype(np.int32)
         didx = torch.from_numpy(idx).to(dev)
-        dst = torch.empty((2, H * r, d), dtype=torch.int16, device=dev)
-        moved = 2 * H * r * row_bytes
+        nsel = len(idx)
+        dst = torch.empty((2, nsel, d), dtype=torch.int16, device=dev)
+        moved = 2 * nsel * row_bytes
         line = {"rows_per_head": r, "heads": H, "bytes": moved, "n": n, "hugepages": args.huge}
         for name, engine in (("lsu", 0), ("tma", 1)):
             best = None
@@ -89,7 +93,7 @@ def main():
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 for m in range(2):
-                    _lib.check(lib.clo_gather_rows_ex(ptrs[m], _lib.DTYPE_BF16, d, H * n, didx.data_ptr(), H * r,
+                    _lib.check(lib.clo_gather_rows_ex(ptrs[m], _lib.DTYPE_BF16, d, H * n, didx.data_ptr(), nsel,
                                                       dst[m].data_ptr(), engine, args.ctas, err.data_ptr(), sp))
                 b.record(stream)
                 torch.cuda.synchronize()
@@ -100,7 +104,7 @@ def main():
             # bit-exact check against the host rows
             hk = np.frombuffer((C.c_char * nbytes).from_address(ptrs[0]), dtype=np.uint16).reshape(H * n, d)
             got = dst[0].cpu().numpy().view(np.uint16)
-            sample = np.arange(0, H * r, max(1, (H * r) // 257))
+            sample = np.arange(0, nsel, max(1, nsel // 257))
             assert np.array_equal(got[sample], hk[idx[sample]]), name
             line[f"{name}_ms"] = best
             line[f"{name}_gbs"] = moved / (best * 1e-3) / 1e9
@@ -112,14 +116,14 @@ def main():
             print(json.dumps(line), flush=True)
             continue
         stg = C.c_void_p()
-        _lib.check(lib.clo_host_alloc(H * r * row_bytes, C.byref(stg)))
+        _lib.check(lib.clo_host_alloc(nsel * row_bytes, C.byref(stg)))
         hidx = np.ascontiguousarray(idx)
         best = None
         for rep in range(min(args.reps, 3) + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for m in range(2):
-                _lib.check(lib.clo_gather_rows_cpu_staged(ptrs[m], _lib.DTYPE_BF16, d, H * n, hidx.ctypes.data, H * r,
+                _lib.check(lib.clo_gather_rows_cpu_staged(ptrs[m], _lib.DTYPE_BF16, d, H * n, hidx.ctypes.data, nsel,
                                                           stg.value, dst[m].data_ptr(), args.threads, sp))
                 torch.cuda.synchronize()
             el = time.perf_counter() - t0
