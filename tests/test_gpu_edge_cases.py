@@ -82,3 +82,22 @@ def test_invalid_configs_raise():
     case["cfg"].policy = "lru"  # block caches are outside the path
     with pytest.raises(ConfigError):
         gpu_engine(case)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 8])
+@pytest.mark.parametrize("d", [64, 128])
+def test_tensor_core_attention_group_sizes(oracle, m, d):
+    """The mma.sync attention (bf16, d 64/128) for every GQA group size the
+    A tile carries (rows 0..m-1 hi, 8..8+m-1 lo), against the fp64 oracle."""
+    case = make_case(L=2, hq=2 * m, hkv=2, d=d, n_prompt=400, steps=4, k=48, batch=2, kv_dtype="bf16",
+                     sink=4, recent=64)
+    run_and_compare(case, oracle)
+
+
+def test_tensor_core_attention_flat_split(oracle):
+    """B*H = 320 heads > 2 x 148: the attention leaves the head-aligned layout
+    for the flat split (segments straddle heads, per-warp partials merged by
+    the last warp of each head)."""
+    case = make_case(L=2, hq=32, hkv=8, d=64, n_prompt=260, steps=3, k=32, batch=40, kv_dtype="bf16",
+                     sink=4, recent=16)
+    run_and_compare(case, oracle)
