@@ -703,16 +703,29 @@ MmaPlan make_plan(const EngineView& v, int W, int ctas_per_sm, int TM) {
 struct MmaShape {
     int warps, stages, ctas, tile;
 };
-MmaShape mma_shape() {
-    static const MmaShape sh = [] {
+// Default: 8 warps x 3 stages, one CTA per SM (measured best, profiles/
+// r1_attention_mma.md) while the heads fit one CTA each (B*H <= 148); with
+// 148 < B*H <= 296 two 4-warp CTAs per SM keep one head per CTA (shared-
+// memory merge, one wave) instead of the flat split.
+MmaShape mma_shape(int heads) {
+    static const int forced = [] {
         const char* e = getenv("CLO_ATTN_SHAPE");  // warps x stages x CTAs/SM x tile rows
         const std::string x = e ? e : "";
-        if (x == "4x3x2x16") return MmaShape{4, 3, 2, 16};
-        if (x == "4x3x1x32") return MmaShape{4, 3, 1, 32};
-        if (x == "4x6x1x16") return MmaShape{4, 6, 1, 16};
-        return MmaShape{8, 3, 1, 16};  // measured best on B200 (profiles/r1_attention_mma.md)
+        if (x == "4x3x2x16") return 1;
+        if (x == "4x3x1x32") return 2;
+        if (x == "4x6x1x16") return 3;
+        if (x == "8x3x1x16") return 4;
+        return 0;
     }();
-    return sh;
+    switch (forced) {
+        case 1: return MmaShape{4, 3, 2, 16};
+        case 2: return MmaShape{4, 3, 1, 32};
+        case 3: return MmaShape{4, 6, 1, 16};
+        case 4: return MmaShape{8, 3, 1, 16};
+        default: break;
+    }
+    if (heads > kNumSMs && heads <= 2 * kNumSMs) return MmaShape{4, 3, 2, 16};
+    return MmaShape{8, 3, 1, 16};
 }
 
 template <int D, int M, int W, int S, int C, int TM, int RC>
@@ -750,7 +763,7 @@ void launch_mma_shape(const EngineView& v, int layer, cudaStream_t stream) {
 
 template <int D, int M>
 void launch_mma(const EngineView& v, int layer, cudaStream_t stream) {
-    const MmaShape sh = mma_shape();
+    const MmaShape sh = mma_shape(v.B * v.H);
     if (sh.tile == 32) {
         launch_mma_shape<D, M, 4, 3, 1, 32>(v, layer, stream);
     } else if (sh.warps == 8) {
