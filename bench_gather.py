@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--huge", action="store_true", help="hugepage-backed pinned host store")
     ap.add_argument("--d", type=int, default=128, help="row width in bf16 elements (256 = K|V interleaved row)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--kv-one-launch", action="store_true",
+                    help="K and V of the selected rows in ONE launch over one 2x store (the engine's access pattern)")
     ap.add_argument("--active", type=int, default=0,
                     help="gather from only this many (random) heads of the store (0 = all)")
     args = ap.parse_args()
@@ -87,6 +89,25 @@ def main():
         dst = torch.empty((2, nsel, d), dtype=torch.int16, device=dev)
         moved = 2 * nsel * row_bytes
         line = {"rows_per_head": r, "heads": H, "bytes": moved, "n": n, "hugepages": args.huge}
+        if args.kv_one_launch:  # one store [2][H*n] rows: indices into K then V halves, one launch
+            if not hasattr(main, "_kv"):
+                p = C.c_void_p()
+                _lib.check(lib.clo_host_alloc(2 * nbytes, C.byref(p)))
+                main._kv = p.value
+            didx2 = torch.cat([didx, didx + H * n])
+            dst2 = torch.empty((2 * nsel, d), dtype=torch.int16, device=dev)
+            best = None
+            for rep in range(args.reps + 1):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                _lib.check(lib.clo_gather_rows_ex(main._kv, _lib.DTYPE_BF16, d, 2 * H * n, didx2.data_ptr(), 2 * nsel,
+                                                  dst2.data_ptr(), 0, args.ctas, err.data_ptr(), sp))
+                b.record(stream)
+                torch.cuda.synchronize()
+                if rep:
+                    best = a.elapsed_time(b) if best is None else min(best, a.elapsed_time(b))
+            line["kv1_ms"] = best
+            line["kv1_gbs"] = moved / (best * 1e-3) / 1e9
         for name, engine in (("lsu", 0), ("tma", 1)):
             best = None
             for rep in range(args.reps + 1):
