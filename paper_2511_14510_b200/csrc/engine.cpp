@@ -30,10 +30,10 @@ namespace {
 // Gather CTAs: enough outstanding PCIe reads to cover the host round trip
 // without flooding the SMs the concurrent kernels need (CLO_GATHER_CTAS
 // overrides for experiments).
-int64_t gather_ctas() {
+int64_t gather_ctas() {  // CLO_GATHER_CTAS: override of the gather grid (0 = the variant's default)
     static const int64_t n = [] {
         const char* e = getenv("CLO_GATHER_CTAS");
-        return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)48;
+        return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)0;
     }();
     return n;
 }
@@ -593,14 +593,8 @@ GatherEngineArgs Engine::gather_args(int layer, int count_bytes) const {
 
 void Engine::enqueue_gather(int layer, int count_bytes, cudaStream_t st) {
     const GatherEngineArgs ga = gather_args(layer, count_bytes);
-    const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
-    const int64_t vecs = (int64_t)cfg_.k * cfg_.shape.head_dim * esz / 16;
-    const int64_t units = (int64_t)ga.items_cap * 2 * ((vecs + 2047) / 2048);
     prof_begin(st);
-    // PCIe needs ~100 KB in flight (55 GB/s x ~2 us); each CTA keeps 32 KiB
-    // outstanding, so a few dozen CTAs saturate the link and leave the SMs to
-    // the selection and attention kernels running concurrently.
-    launch_gather_engine(ga, (int)std::min<int64_t>(units, gather_ctas()), st);
+    launch_gather_engine(ga, (int)gather_ctas(), st);  // picks the copy variant and its grid (gather.cu)
     prof_end(st, "gather_zero_copy", layer);
     launches_ += 1;
 }
@@ -856,7 +850,7 @@ void Engine::capture_graph(int mode) {
         // layer's fetch list as soon as the selection stream publishes it
         if (n_off_layers_ > 0 && flags) {
             launch_gather_persistent(gather_args(0, 1), d_off_layers_.as<int>(), n_off_layers_,
-                                     (int)gather_ctas(), s_xfer);
+                                     gather_ctas() > 0 ? (int)gather_ctas() : 48, s_xfer);
             launches_ += 1;
         }
     }

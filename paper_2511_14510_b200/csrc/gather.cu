@@ -16,6 +16,8 @@
 //              in flight per CTA) and store them into their slots.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -178,6 +180,56 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
         if (e < v1) dst[dsto[uu]] = r[uu];
     }
     if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+}
+
+// Light variant of the engine gather (CLO_GATHER=lite): the same LSU copy
+// with T threads x U 16-byte loads in flight per CTA and 32-bit slot offsets,
+// sized (registers, no shared memory) to co-reside on an SM with one
+// attention CTA, so the transfer stream's CTAs do not take whole SMs away from
+// the compute stream. Unit = (missed head, matrix, T*U vectors).
+template <int T, int U>
+__global__ void __launch_bounds__(T) gather_lite_kernel(const __grid_constant__ GatherEngineArgs a) {
+    const EngineView& v = a.v;
+    const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int vpr = row_bytes / 16;
+    constexpr int kVecs = T * U;
+    const int parts = (v.k * vpr + kVecs - 1) / kVecs;
+    const int upi = 2 * parts;
+    const int units = a.count[a.layer] * upi;
+    const size_t esz = dtype_size(v.kv_dtype);
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / upi, rem = u - item * upi;
+        const int mat = rem / parts, part = rem - mat * parts;
+        const size_t li = (size_t)a.layer * a.items_cap + item;
+        const int v0 = part * kVecs;
+        const int v1 = min(a.fetch_count[li] * vpr, v0 + kVecs);
+        if (v0 >= v1) continue;
+        const int seg = a.items[li].seg;
+        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+        const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+        const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
+        uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.k * row_bytes);
+        const int32_t* ftok = a.fetch_tok + li * v.k;
+        const int32_t* fslot = a.fetch_slot + li * v.k;
+        uint4 r[U];
+        int dsto[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int e = v0 + uu * T + (int)threadIdx.x;
+            if (e < v1) {
+                const int row = e / vpr, c = e - row * vpr;
+                dsto[uu] = fslot[row] * vpr + c;
+                r[uu] = src[(size_t)ftok[row] * vpr + c];
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int e = v0 + uu * T + (int)threadIdx.x;
+            if (e < v1) dst[dsto[uu]] = r[uu];
+        }
+        if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+    }
 }
 
 // One launch per layer (prefill, and the serialised profiling graph).
@@ -362,21 +414,23 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const char* __restrict__
 // whole row) from pinned host memory into a shared-memory stage, completion on
 // an mbarrier, then bulk-stores it to its HBM slot. kTmaStages groups per warp
 // in flight. Groups are (missed head, matrix, 32-row block) of the layer.
-constexpr int kTmaWarps = 4;
+constexpr int kTmaWarps = 4;  // max warps per CTA
+constexpr int kTmaMaxStages = 8;
 
-__global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(GatherEngineArgs a) {
-    extern __shared__ __align__(128) char tstage[];  // [warp][kTmaStages][32][row_bytes]
-    __shared__ __align__(8) uint64_t tbar[kTmaWarps][kTmaStages];
+__global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(GatherEngineArgs a, int stages) {
+    extern __shared__ __align__(128) char tstage[];  // [warp][stages][32][row_bytes]
+    __shared__ __align__(8) uint64_t tbar[kTmaWarps][kTmaMaxStages];
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gpm = (v.k + kTmaRows - 1) / kTmaRows;  // 32-row groups per matrix
     const int total = a.count[a.layer] * 2 * gpm;
-    const int gw = blockIdx.x * kTmaWarps + warp, nw = gridDim.x * kTmaWarps;
+    const int wpc = blockDim.x >> 5;
+    const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
     const int mine = total > gw ? (total - 1 - gw) / nw + 1 : 0;
-    char* st0 = tstage + (size_t)warp * kTmaStages * kTmaRows * row_bytes;
+    char* st0 = tstage + (size_t)warp * stages * kTmaRows * row_bytes;
     if (lane == 0) {
-        for (int s = 0; s < kTmaStages; ++s)
+        for (int s = 0; s < stages; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[warp][s])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -405,7 +459,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         const char* src;
         char* dst;
         locate(i, rows, src, dst);
-        const int s = i % kTmaStages;
+        const int s = i % stages;
         uint64_t* bar = &tbar[warp][s];
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -424,10 +478,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
                 "l"(src), "r"(row_bytes), "r"(smem_u32(bar))
                 : "memory");
     };
-    for (int i = 0; i < min(kTmaStages, mine); ++i) load(i);
+    for (int i = 0; i < min(stages, mine); ++i) load(i);
     unsigned long long moved = 0;
     for (int i = 0; i < mine; ++i) {
-        const int s = i % kTmaStages;
+        const int s = i % stages;
         int rows;
         const char* src;
         char* dst;
@@ -436,7 +490,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             "{\n\t.reg .pred p;\n\tW_%=:\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
             "@!p bra W_%=;\n\t}" ::"r"(smem_u32(&tbar[warp][s])),
-            "r"((i / kTmaStages) & 1)
+            "r"((i / stages) & 1)
             : "memory");
         if (lane < rows) {
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
@@ -447,7 +501,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         }
         moved += (unsigned long long)rows * row_bytes;
         __syncwarp();
-        if (i + kTmaStages < mine) load(i + kTmaStages);
+        if (i + stages < mine) load(i + stages);
     }
     if (lane < 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (a.count_bytes && lane == 0 && moved) atomicAdd(v.gathered_bytes, moved);
@@ -473,19 +527,75 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
     reconcile_kernel<<<grid, kRecThreads, sm, stream>>>(a);
 }
 
-void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream) {
-    static const bool tma = [] {
+// Copy variant by host-region size (measured, profiles/README.md): with
+// per-head host regions up to 48 MiB (128K rows of 256 B) the TMA bulk copy
+// (1 warp, 1 stage of 32 rows = 8 KiB shared memory, one CTA per SM) wins: its
+// CTAs hold no registers for data in flight and co-reside with the attention
+// and selection CTAs (configs[1]: +3.5%; 64K x 32 sequences: +24%). Over larger
+// regions, where each row's host-address translation misses, the LSU copy
+// (48 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
+// outstanding and wins (512K: +8%, 1M: +20%).
+// CLO_GATHER=lsu|tma|lite[:T,U] forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
+void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stream) {
+    static const int mode = [] {  // 0 auto, 1 lsu, 2 tma, else lite T*100+U
         const char* e = getenv("CLO_GATHER");
-        return e && std::string(e) == "tma";
+        if (!e || !*e) return 0;
+        const std::string m(e);
+        if (m == "lsu") return 1;
+        if (m == "tma") return 2;
+        if (m.rfind("lite", 0) == 0) {
+            int t = 128, u = 8;
+            sscanf(e, "lite:%d,%d", &t, &u);
+            return t * 100 + u;
+        }
+        return 0;
     }();
-    const int row_bytes = a.v.d * dtype_size(a.v.kv_dtype);
-    const size_t sm = (size_t)kTmaWarps * kTmaStages * kTmaRows * row_bytes;
-    if (tma && sm <= 200 * 1024) {  // rows up to 400 B: the ring fits one CTA per SM
-        if (sm > 48 * 1024)
-            cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        gather_engine_tma_kernel<<<grid, kTmaWarps * 32, sm, stream>>>(a);
+    static const int2 shape = [] {
+        int2 r{1, 1};
+        if (const char* e = getenv("CLO_GATHER_TMA_SHAPE")) {
+            int w = 0, st = 0;
+            if (sscanf(e, "%d,%d", &w, &st) == 2 && w >= 1 && w <= kTmaWarps && st >= 1 && st <= kTmaMaxStages)
+                r = int2{w, st};
+        }
+        return r;
+    }();
+    const EngineView& v = a.v;
+    const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int vpr = row_bytes / 16;
+    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * row_bytes;
+    const bool small_region = (int64_t)v.nmax * row_bytes <= (int64_t)48 << 20;  // between the measured 32 / 64 MiB points
+    const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
+    if (use == 2 && sm <= 200 * 1024) {
+        const int64_t groups = (int64_t)a.items_cap * 2 * ((v.k + kTmaRows - 1) / kTmaRows);
+        const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : kNumSMs;  // default: one one-warp CTA per SM
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(warps, groups) / shape.x);
+        cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
         return;
     }
+    if (use > 2) {
+        const int t = use / 100, u = use % 100;
+        const int64_t units = (int64_t)a.items_cap * 2 * ((v.k * vpr + t * u - 1) / (t * u));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : kNumSMs, units));
+        switch (use) {
+            case 12804:
+                gather_lite_kernel<128, 4><<<grid, 128, 0, stream>>>(a);
+                return;
+            case 25604:
+                gather_lite_kernel<256, 4><<<grid, 256, 0, stream>>>(a);
+                return;
+            case 6408:
+                gather_lite_kernel<64, 8><<<grid, 64, 0, stream>>>(a);
+                return;
+            default:
+                gather_lite_kernel<128, 8><<<grid, 128, 0, stream>>>(a);
+                return;
+        }
+    }
+    // PCIe needs well over 100 KB in flight; 48 CTAs x 32 KiB saturate the
+    // link and leave most SMs to the selection and attention kernels.
+    const int64_t units = (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 

@@ -27,3 +27,13 @@ def test_flag_transfer_pipeline_matches_oracle():
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "flags ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("variant", ["lsu", "tma", "lite:128,8", "lite:64,8"])
+def test_gather_variants_match_oracle(variant):
+    """Every engine-gather copy variant (launch_gather_engine picks TMA bulk or
+    LSU by host-region size; CLO_GATHER forces one) moves the same rows."""
+    env = dict(os.environ, CLO_GATHER=variant, PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.replace("flags ok", "variant ok")], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stderr[-3000:]
