@@ -216,16 +216,24 @@ __global__ void __launch_bounds__(1024) threshold_signhash_kernel(SelArgs a) {
         const SelItem it = a.items[item];
         const int nch = num_chunks(it.n);
         const uint32_t* hist = a.chunk_hist + (size_t)item * a.max_chunks * a.nb;
-        for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
-        __syncthreads();
-        // warp w sums chunks w, w + nwarps, ... (coalesced bin rows, independent loads)
-        for (int b0 = 0; b0 < a.nb; b0 += 32) {
-            const int b = b0 + lane;
-            if (b < a.nb) {
+        if (nch <= 64) {  // one thread per bin walks the chunks
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
                 uint32_t s = 0;
+#pragma unroll 8
+                for (int c = 0; c < nch; ++c) s += hist[(size_t)c * a.nb + b];
+                tot[b] = s;
+            }
+        } else {  // long items: warp w sums chunks w, w + nwarps, ... (coalesced bin rows)
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
+            __syncthreads();
+            for (int b0 = 0; b0 < a.nb; b0 += 32) {
+                const int b = b0 + lane;
+                if (b < a.nb) {
+                    uint32_t s = 0;
 #pragma unroll 4
-                for (int c = warp; c < nch; c += nwarps) s += hist[(size_t)c * a.nb + b];
-                if (s) atomicAdd(&tot[b], s);
+                    for (int c = warp; c < nch; c += nwarps) s += hist[(size_t)c * a.nb + b];
+                    if (s) atomicAdd(&tot[b], s);
+                }
             }
         }
         __syncthreads();

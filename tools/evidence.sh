@@ -16,5 +16,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"att
   -o gpurun_out/ev_attn -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"score_signhash" -s 300 -c 1 \
   -o gpurun_out/ev_score -f python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# full capture of one engine gather launch (the first: a prefill layer, 128 heads x 2048 rows)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gather_engine" -c 1 \
+  -o gpurun_out/ev_gather -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 # zero-copy gather sweep (configs[4])
 timeout 900 python bench_gather.py > gpurun_out/ev_gather_sweep.jsonl 2>&1
