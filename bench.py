@@ -236,13 +236,13 @@ def run_reference_arm(args):
     if rank != 0:
         return
     threads = cpu_threads(args)
-    steps = args.warmup + args.steps
-    # bound the sample: at 128K each unit-step costs ~0.2 s of CPU
-    steps = min(steps, args.warmup + 8)
-    cb = reference_sample(args, steps, min(args.warmup, 1), threads)
+    # W warm-up and K timed decode steps of one (sequence, layer, KV head) unit
+    # per host thread: a bounded sample of the batch step (~0.15 s per unit-step
+    # at 128K, ~1.2 s at 1M)
+    cb = reference_sample(args, args.warmup + args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": steps - min(args.warmup, 1), "warmup": min(args.warmup, 1),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * args.batch / cb["value"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.cfg["name"], "batch": args.batch, "ctx": args.ctx,
