@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--kv-layout", default="interleaved", choices=["split", "interleaved"],
+                    help="host K/V layout: separate K and V matrices, or one token's K|V rows contiguous")
     ap.add_argument("--huge", action="store_true",
                     help="back the pinned host KV store with 2 MiB pages (GPU TLB reach for large stores)")
     ap.add_argument("--same-device", action="store_true",
@@ -297,7 +299,7 @@ def run_ours(args):
     t_setup = time.time()
 
     # host KV: one aliased [B][1][H][nmax][d] bf16 buffer pair (see module doc)
-    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge)
+    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge, interleaved=args.kv_layout == "interleaved")
     for b in range(B):
         for arr in (hkv.k, hkv.v):
             x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -589,7 +591,9 @@ def run_ours(args):
                                        f"head-output all-gather)" if shard_heads
                                        else f"request-sharded x{world}"),
                        "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
-                       "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers",
+                       "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
+                                  + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
+                                     else "separate K and V matrices"),
                        "sigma_step": args.sigma, "sigma_layer": args.sigma_layer},
             "hit_ratio": hits / max(1, hits + misses),
             "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms), "max": max(step_ms)},

@@ -143,6 +143,15 @@ clo_status clo_engine_bind_host_kv(clo_engine* e, void* k_host, void* v_host,
                                    int64_t seq_stride, int64_t layer_stride,
                                    int64_t head_stride);
 
+/* Same, with an explicit row stride (elements, >= head_dim; row r at
+ * ... + r*row_stride). row_stride = 2*head_dim with v_host = k_host +
+ * head_dim is the interleaved layout: one token's K and V rows are one
+ * contiguous 2*head_dim run, so a fetched token costs one host page
+ * translation instead of two (profiles/README.md: long contexts). */
+clo_status clo_engine_bind_host_kv_ex(clo_engine* e, void* k_host, void* v_host,
+                                      int64_t seq_stride, int64_t layer_stride,
+                                      int64_t head_stride, int64_t row_stride);
+
 /* prefill() — engine.cpp:163-209. true_q0 [B][L][hq][d] f32: step-0 true
  * queries. Encodes retrieval metadata on the GPU, loads persistent heads into
  * HBM, fills sink/recent windows, selects the step-0 top-k and gathers the

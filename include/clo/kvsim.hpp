@@ -170,8 +170,10 @@ class DecodeEngine {
     DecodeEngine(const DecodeEngine&) = delete;
     DecodeEngine& operator=(const DecodeEngine&) = delete;
 
-    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride) {
-        check(clo_engine_bind_host_kv(e_, k, v, seq_stride, layer_stride, head_stride));
+    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride,
+                      int64_t row_stride = 0) {
+        check(row_stride ? clo_engine_bind_host_kv_ex(e_, k, v, seq_stride, layer_stride, head_stride, row_stride)
+                         : clo_engine_bind_host_kv(e_, k, v, seq_stride, layer_stride, head_stride));
     }
     void prefill(const float* true_q0, bool on_host = true, void* stream = nullptr) {
         check(clo_prefill(e_, true_q0, on_host, stream));

@@ -150,6 +150,7 @@ SIGNATURES = {
     "clo_engine_create": (_I, [C.POINTER(EngineConfigC), _P, _P, _P, C.POINTER(_P)]),
     "clo_engine_destroy": (None, [_P]),
     "clo_engine_bind_host_kv": (_I, [_P, _P, _P, _I64, _I64, _I64]),
+    "clo_engine_bind_host_kv_ex": (_I, [_P, _P, _P, _I64, _I64, _I64, _I64]),
     "clo_prefill": (_I, [_P, _P, _I, _P]),
     "clo_decode_step": (_I, [_P, C.POINTER(StepIO), _P]),
     "clo_engine_synchronize": (_I, [_P]),

@@ -139,7 +139,12 @@ void clo_engine_destroy(clo_engine* e) { delete reinterpret_cast<Engine*>(e); }
 
 clo_status clo_engine_bind_host_kv(clo_engine* e, void* k, void* v, int64_t seq_stride,
                                    int64_t layer_stride, int64_t head_stride) {
-    return guarded([&] { ENG->bind_host_kv(k, v, seq_stride, layer_stride, head_stride); });
+    return guarded([&] { ENG->bind_host_kv(k, v, seq_stride, layer_stride, head_stride, 0); });
+}
+
+clo_status clo_engine_bind_host_kv_ex(clo_engine* e, void* k, void* v, int64_t seq_stride, int64_t layer_stride,
+                                      int64_t head_stride, int64_t row_stride) {
+    return guarded([&] { ENG->bind_host_kv(k, v, seq_stride, layer_stride, head_stride, row_stride); });
 }
 
 clo_status clo_prefill(clo_engine* e, const float* true_q0, int on_host, void* stream) {

@@ -84,10 +84,10 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
         store_row<T>(v.pv, p * v.nmax + row, v.d, vr);
     } else {
         const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-        T* hk = static_cast<T*>(v.host_k_w) + hb;
-        T* hv = static_cast<T*>(v.host_v_w) + hb;
-        store_row<T>(hk, row, v.d, kr);  // zero-copy store into the pinned host store
-        store_row<T>(hv, row, v.d, vr);
+        T* hk = static_cast<T*>(v.host_k_w) + hb + (size_t)row * v.row_stride;
+        T* hv = static_cast<T*>(v.host_v_w) + hb + (size_t)row * v.row_stride;
+        store_row<T>(hk, 0, v.d, kr);  // zero-copy store into the pinned host store
+        store_row<T>(hv, 0, v.d, vr);
         const size_t o = (size_t)b * v.NO + v.oidx[lg];
         const int wrows = v.sink + v.recent;
         if (row < v.sink) {
@@ -159,16 +159,17 @@ __global__ void window_init_kernel(EngineView v) {
     T* wv = static_cast<T*>(v.win_v) + o * wrows * v.d;
     const int ns = min(v.sink, n);
     for (int i = threadIdx.x; i < ns * v.d; i += blockDim.x) {
-        wk[i] = hk[i];
-        wv[i] = hv[i];
+        const size_t src = (size_t)(i / v.d) * v.row_stride + i % v.d;
+        wk[i] = hk[src];
+        wv[i] = hv[src];
     }
     if (v.recent > 0) {
         const int t0 = max(0, n - v.recent);
         for (int i = threadIdx.x; i < (n - t0) * v.d; i += blockDim.x) {
             const int t = t0 + i / v.d, c = i % v.d;
             const size_t dst = (size_t)(v.sink + t % v.recent) * v.d + c;
-            wk[dst] = hk[(size_t)t * v.d + c];
-            wv[dst] = hv[(size_t)t * v.d + c];
+            wk[dst] = hk[(size_t)t * v.row_stride + c];
+            wv[dst] = hv[(size_t)t * v.row_stride + c];
         }
     }
 }

@@ -409,6 +409,7 @@ EngineView Engine::view() const {
     v.seq_stride = seq_stride_;
     v.layer_stride = layer_stride_;
     v.head_stride = head_stride_;
+    v.row_stride = row_stride_ ? row_stride_ : cfg_.shape.head_dim;
     v.persistent = d_persistent_.as<int>();
     v.pidx = d_pidx_.as<int>();
     v.oidx = d_oidx_.as<int>();
@@ -600,7 +601,7 @@ void Engine::enqueue_gather(int layer, int count_bytes, cudaStream_t st) {
 }
 
 void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride,
-                          int64_t head_stride) {
+                          int64_t head_stride, int64_t row_stride) {
     if (!k || !v) fail(CLO_ERR_ARGUMENT, "host K/V pointers must be non-null");
     for (void* p : {k, v}) {
         cudaPointerAttributes at{};
@@ -610,6 +611,14 @@ void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_st
                  "host K/V must be pinned, UVA-mapped memory (clo_host_alloc or cudaHostRegister)");
     }
     if (seq_stride < 0 || layer_stride < 0 || head_stride < 0) fail(CLO_ERR_ARGUMENT, "negative stride");
+    const int d = cfg_.shape.head_dim;
+    const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    if (row_stride == 0) row_stride = d;
+    if (row_stride < d) fail(CLO_ERR_ARGUMENT, "row_stride must be at least head_dim");
+    if (row_stride * esz % 16 != 0) fail(CLO_ERR_ARGUMENT, "row_stride must be a multiple of 16 bytes");
+    for (const void* p : {(const void*)k, (const void*)v})
+        if (reinterpret_cast<uintptr_t>(p) % 16 != 0) fail(CLO_ERR_ARGUMENT, "host K/V must be 16-byte aligned");
+    row_stride_ = row_stride;
     host_k_ = k;
     host_v_ = v;
     seq_stride_ = seq_stride;
@@ -758,8 +767,11 @@ void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
             while (l0 < L) {
                 const int l1 = layer_stride_ == 0 ? L : l0 + 1;  // layers sharing this host buffer
                 const size_t hoff = ((size_t)b * seq_stride_ + (size_t)l0 * layer_stride_ + (size_t)g * head_stride_) * esz;
-                CLO_CUDA(cudaMemcpyAsync(stage_k.p, hk + hoff, (size_t)n * d * esz, cudaMemcpyHostToDevice, st));
-                CLO_CUDA(cudaMemcpyAsync(stage_v.p, hv + hoff, (size_t)n * d * esz, cudaMemcpyHostToDevice, st));
+                const size_t pitch = (size_t)(row_stride_ ? row_stride_ : d) * esz;
+                CLO_CUDA(cudaMemcpy2DAsync(stage_k.p, (size_t)d * esz, hk + hoff, pitch, (size_t)d * esz, n,
+                                           cudaMemcpyHostToDevice, st));
+                CLO_CUDA(cudaMemcpy2DAsync(stage_v.p, (size_t)d * esz, hv + hoff, pitch, (size_t)d * esz, n,
+                                           cudaMemcpyHostToDevice, st));
                 launch_check_finite(stage_k.p, cfg_.kv_dtype, (int64_t)n * d, d_err_.as<int>(), kErrNonFiniteKey, st);
                 launch_check_finite(stage_v.p, cfg_.kv_dtype, (int64_t)n * d, d_err_.as<int>(), kErrNonFiniteValue, st);
                 launches_ += 2;

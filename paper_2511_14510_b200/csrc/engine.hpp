@@ -23,7 +23,8 @@ class Engine {
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
 
-    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride);
+    void bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_stride, int64_t head_stride,
+                      int64_t row_stride);  // row_stride 0 = head_dim
     void prefill(const float* true_q0, int on_host, cudaStream_t user);
     void decode_step(const clo_step_io& io, cudaStream_t user);
     void synchronize();
@@ -88,7 +89,7 @@ class Engine {
 
     void* host_k_ = nullptr;
     void* host_v_ = nullptr;
-    int64_t seq_stride_ = 0, layer_stride_ = 0, head_stride_ = 0;
+    int64_t seq_stride_ = 0, layer_stride_ = 0, head_stride_ = 0, row_stride_ = 0;
 
     DevBuf d_persistent_, d_pidx_, d_oidx_, d_tau_, d_qimp_;
     DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;

@@ -74,6 +74,7 @@ struct EngineView {
     void* host_k_w;        // same pointers, writable (append)
     void* host_v_w;
     int64_t seq_stride, layer_stride, head_stride;
+    int64_t row_stride;  // host elements between consecutive rows of one head (head_dim, or 2*head_dim interleaved)
     // placement
     const int* persistent; // [L*H]
     const int* pidx;       // [L*H] index among persistent (l,g) or -1

@@ -145,6 +145,7 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
+    const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);  // host row pitch
     const int parts = (v.k * vpr + kUnitVecs - 1) / kUnitVecs;  // per matrix
     const int units_per_item = 2 * parts;
     const size_t esz = dtype_size(v.kv_dtype);
@@ -171,7 +172,7 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
         if (e < v1) {
             const int row = e / vpr, c = e - row * vpr;
             dsto[uu] = (size_t)fslot[row] * vpr + c;
-            r[uu] = src[(size_t)ftok[row] * vpr + c];
+            r[uu] = src[(size_t)ftok[row] * rvpr + c];
         }
     }
 #pragma unroll
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(T) gather_lite_kernel(const __grid_constant__ 
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
+    const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);  // host row pitch
     constexpr int kVecs = T * U;
     const int parts = (v.k * vpr + kVecs - 1) / kVecs;
     const int upi = 2 * parts;
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(T) gather_lite_kernel(const __grid_constant__ 
             if (e < v1) {
                 const int row = e / vpr, c = e - row * vpr;
                 dsto[uu] = fslot[row] * vpr + c;
-                r[uu] = src[(size_t)ftok[row] * vpr + c];
+                r[uu] = src[(size_t)ftok[row] * rvpr + c];
             }
         }
 #pragma unroll
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
             const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
             const int r = grp * kTmaRows + lane;
-            src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.d) * dtype_size(v.kv_dtype);
+            src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.row_stride) * dtype_size(v.kv_dtype);
             dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
         }
     };

@@ -132,24 +132,36 @@ def profiles_from_arrays(tau: np.ndarray, q_importance: np.ndarray):
 
 
 class HostKV:
-    """Pinned, UVA-mapped host K/V store [B][Lk][H][nmax][d] (HeadStore::k/v)."""
+    """Pinned, UVA-mapped host K/V store [B][Lk][H][nmax][d] (HeadStore::k/v).
 
-    def __init__(self, batch, layers, heads, nmax, d, kv_dtype, hugepages: bool = False):
+    interleaved=True stores one buffer [B][Lk][H][nmax][2][d]: a token's K and
+    V rows are contiguous (row stride 2d), so fetching it over PCIe touches one
+    host page instead of two. `k` and `v` are strided views either way."""
+
+    def __init__(self, batch, layers, heads, nmax, d, kv_dtype, hugepages: bool = False,
+                 interleaved: bool = False):
         lib = _lib.load()
         self.np_dtype = np.uint16 if kv_dtype == "bf16" else np.float32
         self.shape = (batch, layers, heads, nmax, d)
+        self.interleaved = interleaved
         nbytes = int(np.prod(self.shape)) * np.dtype(self.np_dtype).itemsize
         self._ptrs = []
         arrays = []
-        for _ in range(2):
+        for _ in range(1 if interleaved else 2):
             p = C.c_void_p()
-            check(lib.clo_host_alloc_ex(nbytes, _lib.HOST_HUGEPAGES if hugepages else 0, C.byref(p)))
+            size = 2 * nbytes if interleaved else nbytes
+            check(lib.clo_host_alloc_ex(size, _lib.HOST_HUGEPAGES if hugepages else 0, C.byref(p)))
             self._ptrs.append(p.value)
-            buf = (C.c_char * nbytes).from_address(p.value)
-            arrays.append(np.frombuffer(buf, dtype=self.np_dtype).reshape(self.shape))
-        self.k, self.v = arrays
+            buf = (C.c_char * size).from_address(p.value)
+            arrays.append(np.frombuffer(buf, dtype=self.np_dtype))
+        if interleaved:
+            kv = arrays[0].reshape(self.shape[:4] + (2, d))
+            self.k, self.v = kv[..., 0, :], kv[..., 1, :]
+        else:
+            self.k, self.v = (a.reshape(self.shape) for a in arrays)
         el = np.dtype(self.np_dtype).itemsize
         self.strides = tuple(s // el for s in self.k.strides[:3])  # seq, layer, head (elements)
+        self.row_stride = self.k.strides[3] // el
 
     def close(self):
         lib = _lib.load()
@@ -204,8 +216,8 @@ class DecodeEngine:
             self.hkv.k[:, :, :, : self.n_prompt] = source.prompt_k
             self.hkv.v[:, :, :, : self.n_prompt] = source.prompt_v
         ss, ls, hs = self.hkv.strides
-        check(self.lib.clo_engine_bind_host_kv(self.h, self.hkv.k.ctypes.data, self.hkv.v.ctypes.data,
-                                               ss, 0 if Lk == 1 else ls, hs))
+        check(self.lib.clo_engine_bind_host_kv_ex(self.h, self.hkv.k.ctypes.data, self.hkv.v.ctypes.data,
+                                                  ss, 0 if Lk == 1 else ls, hs, self.hkv.row_stride))
         self.current_step = 0
         self._outputs = []
         self.world = 1

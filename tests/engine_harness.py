@@ -6,7 +6,7 @@ from __future__ import annotations
 import numpy as np
 
 from oracle.bind import EngineCfg
-from paper_2511_14510_b200 import (DecodeEngine, EngineConfig, ModeFlags, ModelShape,
+from paper_2511_14510_b200 import (DecodeEngine, EngineConfig, HostKV, ModeFlags, ModelShape,
                                    PartitionPlan, profiles_from_arrays)
 from paper_2511_14510_b200.workload import Shape, SyntheticWorkload, widen
 
@@ -16,7 +16,7 @@ POLICY_CODE = {"similarity": 0, "prefetch_only": 3}
 def make_case(L=3, hq=4, hkv=2, d=16, n_prompt=96, steps=12, k=8, batch=2, kv_dtype="f32",
               retriever="sign_hash", policy="similarity", sink=2, recent=8, always_miss=False,
               always_hit=False, tau_override=None, persistent=None, seed=5, sigma_step=0.15,
-              hash_bits=256, alias_layers=False, tau=None):
+              hash_bits=256, alias_layers=False, tau=None, interleaved=False):
     shape = Shape(L, hq, hkv, d)
     wl = SyntheticWorkload(shape, batch, n_prompt, steps, kv_dtype=kv_dtype, sigma_step=sigma_step,
                            seed=seed, alias_layers=alias_layers)
@@ -36,7 +36,7 @@ def make_case(L=3, hq=4, hkv=2, d=16, n_prompt=96, steps=12, k=8, batch=2, kv_dt
                        batch=batch, kv_dtype=kv_dtype)
     plan = PartitionPlan(layers=[[g for g in range(hkv) if persistent[l, g]] for l in range(L)])
     return dict(shape=shape, wl=wl, cfg=cfg, plan=plan, tau=tau, qimp=qimp,
-                persistent=np.asarray(persistent, np.int32))
+                persistent=np.asarray(persistent, np.int32), interleaved=interleaved)
 
 
 def oracle_cfg(case) -> EngineCfg:
@@ -57,8 +57,15 @@ def oracle_cfg(case) -> EngineCfg:
 
 
 def gpu_engine(case) -> DecodeEngine:
+    hkv = None
+    if case.get("interleaved"):  # host K|V rows of a token contiguous (row stride 2d)
+        cfg, wl = case["cfg"], case["wl"]
+        s = cfg.shape
+        Lk = 1 if getattr(wl, "alias_layers", False) else s.num_layers
+        hkv = HostKV(cfg.batch, Lk, s.num_kv_heads, wl.n_prompt + wl.steps, s.head_dim, cfg.kv_dtype,
+                     interleaved=True)
     return DecodeEngine(case["cfg"], profiles_from_arrays(case["tau"], case["qimp"]), case["plan"],
-                        case["wl"])
+                        case["wl"], host_kv=hkv)
 
 
 def oracle_engines(case, oracle):

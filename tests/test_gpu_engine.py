@@ -158,3 +158,15 @@ def test_timeline_breakdown_measured():
     doc = _json.loads(b.timeline_json())
     assert doc["steps"] == case["wl"].steps and len(doc["layers"]) == 3
     assert abs(doc["total"]["transfer_s"] - tot["exposed_s"]) <= 1e-9  # the reference's key = exposed
+
+
+@pytest.mark.parametrize("kw", [dict(kv_dtype="f32"), dict(kv_dtype="bf16", d=128, hq=8, hkv=2, n_prompt=400, k=32),
+                                dict(kv_dtype="bf16", alias_layers=True, always_miss=True, retriever="exact"),
+                                dict(kv_dtype="bf16", d=64, persistent=np.eye(3, 2, dtype=np.int32))])
+def test_interleaved_host_layout_matches_oracle(oracle, kw):
+    """Host K|V rows of a token contiguous (clo_engine_bind_host_kv_ex, row
+    stride 2d): prompt staging, window init, appends and every gather variant
+    address the strided rows; results identical to the oracle."""
+    case = make_case(interleaved=True, **kw)
+    g, o, worst = run_and_compare(case, oracle)
+    assert g.hkv.row_stride == 2 * case["cfg"].shape.head_dim
