@@ -410,6 +410,11 @@ EngineView Engine::view() const {
     v.layer_stride = layer_stride_;
     v.head_stride = head_stride_;
     v.row_stride = row_stride_ ? row_stride_ : cfg_.shape.head_dim;
+    {
+        const int64_t d = cfg_.shape.head_dim, esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+        v.kv_fused = host_k_ && v.row_stride == 2 * d &&
+                     static_cast<const char*>(host_v_) == static_cast<const char*>(host_k_) + d * esz;
+    }
     v.persistent = d_persistent_.as<int>();
     v.pidx = d_pidx_.as<int>();
     v.oidx = d_oidx_.as<int>();

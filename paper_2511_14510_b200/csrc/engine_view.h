@@ -75,6 +75,7 @@ struct EngineView {
     void* host_v_w;
     int64_t seq_stride, layer_stride, head_stride;
     int64_t row_stride;  // host elements between consecutive rows of one head (head_dim, or 2*head_dim interleaved)
+    int kv_fused;        // interleaved host K|V (host_v = host_k + d, row_stride = 2d): gather a token's K|V run at once
     // placement
     const int* persistent; // [L*H]
     const int* pidx;       // [L*H] index among persistent (l,g) or -1

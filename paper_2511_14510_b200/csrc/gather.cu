@@ -135,8 +135,11 @@ __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a)
 // Work units = (missed head, matrix, block of fetch-list vectors). K and V are
 // separate units (all of a head's K rows, then its V rows) so a CTA's
 // outstanding reads stay within one host matrix region at a time.
+// Interleaved host K|V (v.kv_fused): one unit covers whole 2*d-element token
+// runs, split into the K and V slots on the way out.
 __device__ __forceinline__ int gather_units_per_item(const EngineView& v) {
     const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
+    if (v.kv_fused) return (v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs;
     return 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
 }
 
@@ -146,6 +149,42 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
     const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);  // host row pitch
+    if (v.kv_fused) {  // token runs [K row | V row] of 2*vpr vectors
+        const int vpt = 2 * vpr;
+        const int upi = (v.k * vpt + kUnitVecs - 1) / kUnitVecs;
+        const int item = u / upi, part = u % upi;
+        const size_t li = (size_t)layer * a.items_cap + item;
+        const int v0 = part * kUnitVecs;
+        const int v1 = min(a.fetch_count[li] * vpt, v0 + kUnitVecs);
+        if (v0 >= v1) return;
+        const int seg = a.items[li].seg;
+        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+        const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+        const uint4* src = reinterpret_cast<const uint4*>((const char*)v.host_k + base * dtype_size(v.kv_dtype));
+        uint4* dk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.k * row_bytes);
+        uint4* dv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.k * row_bytes);
+        const int32_t* ftok = a.fetch_tok + li * v.k;
+        const int32_t* fslot = a.fetch_slot + li * v.k;
+        uint4 r[kUnitUnroll];
+        uint4* dp[kUnitUnroll];
+#pragma unroll
+        for (int uu = 0; uu < kUnitUnroll; ++uu) {
+            const int e = v0 + uu * kGatherThreads + threadIdx.x;
+            if (e < v1) {
+                const int row = e / vpt, c = e - row * vpt;
+                dp[uu] = c < vpr ? dk + (size_t)fslot[row] * vpr + c : dv + (size_t)fslot[row] * vpr + (c - vpr);
+                r[uu] = src[(size_t)ftok[row] * rvpr + c];
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < kUnitUnroll; ++uu) {
+            const int e = v0 + uu * kGatherThreads + threadIdx.x;
+            if (e < v1) *dp[uu] = r[uu];
+        }
+        if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+        return;
+    }
     const int parts = (v.k * vpr + kUnitVecs - 1) / kUnitVecs;  // per matrix
     const int units_per_item = 2 * parts;
     const size_t esz = dtype_size(v.kv_dtype);
@@ -426,11 +465,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gpm = (v.k + kTmaRows - 1) / kTmaRows;  // 32-row groups per matrix
-    const int total = a.count[a.layer] * 2 * gpm;
+    const bool fused = v.kv_fused;                    // one [K|V] token run per lane and group
+    const int nmat = fused ? 1 : 2;
+    const int cbytes = fused ? 2 * row_bytes : row_bytes;  // bytes copied per row
+    const int total = a.count[a.layer] * nmat * gpm;
     const int wpc = blockDim.x >> 5;
     const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
     const int mine = total > gw ? (total - 1 - gw) / nw + 1 : 0;
-    char* st0 = tstage + (size_t)warp * stages * kTmaRows * row_bytes;
+    char* st0 = tstage + (size_t)warp * stages * kTmaRows * cbytes;
     if (lane == 0) {
         for (int s = 0; s < stages; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[warp][s])));
@@ -438,14 +480,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     }
     __syncwarp();
     // group i of this warp -> (rows, host source of lane's row, slot destination)
-    auto locate = [&](int i, int& rows, const char*& src, char*& dst) {
+    auto locate = [&](int i, int& rows, const char*& src, char*& dst, char*& dst2) {
         const int gidx = gw + i * nw;
-        const int item = gidx / (2 * gpm), rem = gidx % (2 * gpm), mat = rem / gpm, grp = rem % gpm;
+        const int item = gidx / (nmat * gpm), rem = gidx % (nmat * gpm), mat = rem / gpm, grp = rem % gpm;
         const size_t li = (size_t)a.layer * a.items_cap + item;
         const int nf = a.fetch_count[li];
         rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
         src = nullptr;
         dst = nullptr;
+        dst2 = nullptr;
         if (lane < rows) {
             const int seg = a.items[li].seg;
             const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
@@ -454,20 +497,21 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             const int r = grp * kTmaRows + lane;
             src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.row_stride) * dtype_size(v.kv_dtype);
             dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
+            if (fused) dst2 = (char*)v.slot_v + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
         }
     };
     auto load = [&](int i) {
         int rows;
         const char* src;
-        char* dst;
-        locate(i, rows, src, dst);
+        char *dst, *dst2;
+        locate(i, rows, src, dst, dst2);
         const int s = i % stages;
         uint64_t* bar = &tbar[warp][s];
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (rows)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                             "r"(rows * row_bytes)
+                             "r"(rows * cbytes)
                              : "memory");
             else
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -476,8 +520,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         if (lane < rows)
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_u32(st0 + ((size_t)s * kTmaRows + lane) * row_bytes)),
-                "l"(src), "r"(row_bytes), "r"(smem_u32(bar))
+                    smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes)),
+                "l"(src), "r"(cbytes), "r"(smem_u32(bar))
                 : "memory");
     };
     for (int i = 0; i < min(stages, mine); ++i) load(i);
@@ -486,8 +530,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         const int s = i % stages;
         int rows;
         const char* src;
-        char* dst;
-        locate(i, rows, src, dst);
+        char *dst, *dst2;
+        locate(i, rows, src, dst, dst2);
         asm volatile(
             "{\n\t.reg .pred p;\n\tW_%=:\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -495,13 +539,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             "r"((i / stages) & 1)
             : "memory");
         if (lane < rows) {
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                         "r"(smem_u32(st0 + ((size_t)s * kTmaRows + lane) * row_bytes)), "r"(row_bytes)
+            const uint32_t sa = smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa),
+                         "r"(row_bytes)
                          : "memory");
+            if (fused)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst2),
+                             "r"(sa + row_bytes), "r"(row_bytes)
+                             : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage reusable
         }
-        moved += (unsigned long long)rows * row_bytes;
+        moved += (unsigned long long)rows * cbytes;
         __syncwarp();
         if (i + stages < mine) load(i + stages);
     }
@@ -564,11 +613,12 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
-    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * row_bytes;
+    const int cbytes = v.kv_fused ? 2 * row_bytes : row_bytes;
+    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * cbytes;
     const bool small_region = (int64_t)v.nmax * row_bytes <= (int64_t)48 << 20;  // between the measured 32 / 64 MiB points
     const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
     if (use == 2 && sm <= 200 * 1024) {
-        const int64_t groups = (int64_t)a.items_cap * 2 * ((v.k + kTmaRows - 1) / kTmaRows);
+        const int64_t groups = (int64_t)a.items_cap * (v.kv_fused ? 1 : 2) * ((v.k + kTmaRows - 1) / kTmaRows);
         const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : kNumSMs;  // default: one one-warp CTA per SM
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(warps, groups) / shape.x);
         cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -596,7 +646,8 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     }
     // PCIe needs well over 100 KB in flight; 48 CTAs x 32 KiB saturate the
     // link and leave most SMs to the selection and attention kernels.
-    const int64_t units = (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
+    const int64_t units = v.kv_fused ? (int64_t)a.items_cap * ((v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs)
+                                     : (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }

@@ -16,7 +16,9 @@ SCRIPT = """
 from oracle.bind import Oracle
 from tests.engine_harness import make_case, run_and_compare
 for kw in (dict(), dict(kv_dtype="bf16", d=128, hq=8, hkv=2, n_prompt=400, k=32, sink=4, recent=64),
-           dict(policy="prefetch_only"), dict(always_miss=True, retriever="exact")):
+           dict(policy="prefetch_only"), dict(always_miss=True, retriever="exact"),
+           dict(kv_dtype="bf16", d=128, hq=8, hkv=2, n_prompt=400, k=32, interleaved=True),
+           dict(kv_dtype="f32", always_miss=True, interleaved=True)):
     run_and_compare(make_case(**kw), Oracle())
 print("flags ok")
 """
