@@ -580,7 +580,7 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 
 // Copy variant by host-region size (measured, profiles/README.md): with
 // per-head host regions up to 48 MiB (128K rows of 256 B) the TMA bulk copy
-// (1 warp, 1 stage of 32 rows = 8 KiB shared memory, one CTA per SM) wins: its
+// (1 warp, 1 stage of 32 rows = 8 KiB shared memory, 128 CTAs) wins: its
 // CTAs hold no registers for data in flight and co-reside with the attention
 // and selection CTAs (configs[1]: +3.5%; 64K x 32 sequences: +24%). Over larger
 // regions, where each row's host-address translation misses, the LSU copy
@@ -619,7 +619,7 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
     if (use == 2 && sm <= 200 * 1024) {
         const int64_t groups = (int64_t)a.items_cap * (v.kv_fused ? 1 : 2) * ((v.k + kTmaRows - 1) / kTmaRows);
-        const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : kNumSMs;  // default: one one-warp CTA per SM
+        const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : 128;  // measured: 128 one-warp CTAs
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(warps, groups) / shape.x);
         cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
