@@ -408,6 +408,7 @@ clo_status clo_group_topk(const double* queries_dev, int m, int d, int retriever
         a.dtype = dtype;
         a.q64 = queries_dev;
         a.grid = std::min(max_chunks, kNumSMs * 8);
+        a.max_items = 1;
         base.alloc(sizeof(int) * max_chunks, false);
         take.alloc(sizeof(int) * max_chunks, false);
         thresh.alloc(sizeof(uint64_t));

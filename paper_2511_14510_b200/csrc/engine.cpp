@@ -502,6 +502,7 @@ SelArgs Engine::sel_args(int which, int layer) const {
     a.need = sc.need;
     a.radix_hist = sc.radix_hist;
     a.grid = grid_for((int64_t)cfg_.batch * s.num_kv_heads * max_chunks_);
+    a.max_items = cfg_.batch * s.num_kv_heads;
     return a;
 }
 

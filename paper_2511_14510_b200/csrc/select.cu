@@ -608,7 +608,8 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
             break;
     }
     const size_t sm_thr = (size_t)a.nb * 4 + (size_t)a.max_chunks * 8;
-    int items_grid = a.grid < 1024 ? a.grid : 1024;
+    // one CTA per item (the kernels grid-stride over *count <= max_items)
+    const int items_grid = a.max_items > 0 ? (a.max_items < 1024 ? a.max_items : 1024) : (a.grid < 1024 ? a.grid : 1024);
     threshold_signhash_kernel<<<items_grid, 1024, sm_thr, stream>>>(a);
     compact_kernel<uint16_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
 }
@@ -626,7 +627,8 @@ void launch_select_exact(const SelArgs& a, cudaStream_t stream) {
             score_exact_kernel<double><<<a.grid, kScoreThreads, sm_q, stream>>>(a);
             break;
     }
-    int items_grid = a.grid < 1024 ? a.grid : 1024;
+    // one CTA per item (the kernels grid-stride over *count <= max_items)
+    const int items_grid = a.max_items > 0 ? (a.max_items < 1024 ? a.max_items : 1024) : (a.grid < 1024 ? a.grid : 1024);
     for (int shift = 56; shift >= 0; shift -= 8) {
         radix_hist_kernel<<<a.grid, kScoreThreads, 0, stream>>>(a, shift);
         radix_pick_kernel<<<items_grid, 32, 0, stream>>>(a, shift);

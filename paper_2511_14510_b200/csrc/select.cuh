@@ -45,6 +45,7 @@ struct SelArgs {
     int* need;              // [item]
     uint32_t* radix_hist;   // [item][256]
     int grid;               // CTAs for the grid-stride kernels
+    int max_items;          // host-side upper bound of *count (sizes the per-item grids)
 };
 
 // Host launchers (select.cu). All enqueue on `stream`; no host sync.
