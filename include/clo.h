@@ -136,7 +136,13 @@ void clo_engine_destroy(clo_engine* e);
  * cudaHostRegister'ed), row-major rows of head_dim elements of kv_dtype.
  * Row r of (seq b, layer l, kv head g) lives at
  *   base + b*seq_stride + l*layer_stride + g*head_stride + r*head_dim
- * (strides in elements). layer_stride 0 aliases one buffer across layers.
+ * (strides in elements; seq/layer/head strides must be multiples of 16
+ * bytes). layer_stride 0 aliases one buffer across layers: every layer then
+ * reads the same prompt rows, and each decode step must append the SAME new
+ * K/V row to every layer of a (seq, kv head) — the engine checks that on the
+ * device and reports CLO_ERR_CONTRACT at the next synchronising call when a
+ * step's rows differ between layers. Bind before clo_prefill (rebinding
+ * afterwards is a CLO_ERR_CONTRACT).
  * Rows [0, n_prompt) must hold the prompt before clo_prefill; decode steps
  * append row n_prompt + t - 1 at step t. */
 clo_status clo_engine_bind_host_kv(clo_engine* e, void* k_host, void* v_host,
@@ -175,6 +181,8 @@ typedef struct clo_step_io {
  * buffers give full overlap). Errors detected on the device (non-finite
  * inputs, ContractError guards) are reported by the next synchronising call. */
 clo_status clo_decode_step(clo_engine* e, const clo_step_io* io, void* stream);
+/* Steps may be issued on different streams; each step is ordered after the
+ * previous one (an event recorded after every step's graph). */
 
 /* Blocks until every queued step finished; returns a deferred device error. */
 clo_status clo_engine_synchronize(clo_engine* e);

@@ -68,6 +68,7 @@ enum ErrBits : int {
     kErrContract = 32,
     kErrInternal = 64,
     kErrExchange = 128,  // head-output exchange: a peer stopped arriving
+    kErrAlias = 256,     // layer-aliased host store: a step's new K/V rows differ across layers
 };
 
 __device__ __forceinline__ void raise_err(int* flag, int bits) {

@@ -50,6 +50,14 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const EncodeSeg* se
 }
 
 template <typename T>
+__device__ __forceinline__ bool same_bits(T a, T b) {
+    if constexpr (sizeof(T) == 2)
+        return __bfloat16_as_ushort(a) == __bfloat16_as_ushort(b);
+    else
+        return __float_as_uint(a) == __float_as_uint(b);
+}
+
+template <typename T>
 __device__ __forceinline__ void store_row(void* base, size_t row, int d, const T* src) {
     T* dst = static_cast<T*>(base) + row * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
@@ -86,8 +94,28 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
         const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
         T* hk = static_cast<T*>(v.host_k_w) + hb + (size_t)row * v.row_stride;
         T* hv = static_cast<T*>(v.host_v_w) + hb + (size_t)row * v.row_stride;
-        store_row<T>(hk, 0, v.d, kr);  // zero-copy store into the pinned host store
-        store_row<T>(hv, 0, v.d, vr);
+        // layer_stride 0 aliases one host matrix across layers: sound only if
+        // every layer appends the same row. Layer 0 (or the first offloaded
+        // layer) writes it; later layers check their step input against layer
+        // 0's (device memory) and raise kErrAlias instead of overwriting it.
+        bool write = true;
+        if (v.layer_stride == 0 && l > 0) {
+            const size_t off0 = ((size_t)b * v.L * v.H + g) * v.d;  // layer 0, same (b, g)
+            const T* nk0 = static_cast<const T*>(v.desc->new_k) + off0;
+            const T* nv0 = static_cast<const T*>(v.desc->new_v) + off0;
+            int diff = 0;
+            for (int i = threadIdx.x; i < v.d; i += blockDim.x)
+                diff |= !same_bits<T>(nk0[i], kr[i]) || !same_bits<T>(nv0[i], vr[i]);
+            if (__syncthreads_or(diff)) {
+                if (threadIdx.x == 0) raise_err(v.err, kErrAlias);
+            }
+            for (int l2 = 0; l2 < l && write; ++l2)  // the first offloaded layer of head g writes the row
+                write = v.persistent[l2 * v.H + g] != 0;
+        }
+        if (write) {
+            store_row<T>(hk, 0, v.d, kr);  // zero-copy store into the pinned host store
+            store_row<T>(hv, 0, v.d, vr);
+        }
         const size_t o = (size_t)b * v.NO + v.oidx[lg];
         const int wrows = v.sink + v.recent;
         if (row < v.sink) {
@@ -101,7 +129,7 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
         if (v.kmirror) store_row<T>(v.kmirror, o * v.nmax + row, v.d, kr);
     }
     if (v.retriever == 1) {
-        uint32_t* out32 = reinterpret_cast<uint32_t*>(v.codes + ((size_t)seg * v.nmax + row) * v.words);
+        uint32_t* out32 = reinterpret_cast<uint32_t*>(v.codes + (size_t)seg * v.code_stride + (size_t)row * v.words);
         const double* pt = v.proj_t + (size_t)lg * v.d * v.bits;
         for (int b0 = 0; b0 < v.words * 64; b0 += blockDim.x) {
             const int bit = b0 + threadIdx.x;

@@ -159,6 +159,7 @@ Engine::~Engine() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_join2_) cudaEventDestroy(ev_join2_);
+    if (ev_step_) cudaEventDestroy(ev_step_);
     if (s_main_) cudaStreamDestroy(s_main_);
     if (s_pref_) cudaStreamDestroy(s_pref_);
     if (s_xfer_) cudaStreamDestroy(s_xfer_);
@@ -179,6 +180,7 @@ void Engine::allocate() {
     nmax_ = cfg_.n_prompt + cfg_.max_steps;
     max_chunks_ = (nmax_ + kScoreChunk - 1) / kScoreChunk;
     words_ = (cfg_.hash_bits + 63) / 64;
+    code_stride_ = ((int64_t)nmax_ * words_ + 1) / 2 * 2;
     nb_ = cfg_.hash_bits + 1;
     const size_t segs = (size_t)B * L * H;
     const size_t wrows = (size_t)cfg_.sink_tokens + cfg_.recent_tokens;
@@ -205,7 +207,7 @@ void Engine::allocate() {
     d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
     d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k + 64);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
-        d_codes_.alloc(sizeof(uint64_t) * segs * nmax_ * words_ + 64, false);
+        d_codes_.alloc(sizeof(uint64_t) * segs * code_stride_ + 64, false);
         // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
         // (engine.cpp:172-174); stored transposed [d][bits] for coalesced reads.
         std::vector<double> pt((size_t)L * H * d * cfg_.hash_bits);
@@ -429,6 +431,7 @@ EngineView Engine::view() const {
     v.entry_slot = d_entry_slot_.as<int32_t>();
     v.slot_tok = d_slot_tok_.as<int32_t>();
     v.codes = d_codes_.as<uint64_t>();
+    v.code_stride = code_stride_;
     v.proj_t = d_proj_t_.as<double>();
     v.labels = d_labels_.as<double>();
     v.label_valid = d_label_valid_.as<int>();
@@ -616,9 +619,12 @@ void Engine::bind_host_kv(void* k, void* v, int64_t seq_stride, int64_t layer_st
             fail(CLO_ERR_ARGUMENT,
                  "host K/V must be pinned, UVA-mapped memory (clo_host_alloc or cudaHostRegister)");
     }
+    if (prefilled_) fail(CLO_ERR_CONTRACT, "bind the host K/V store before prefill, not after");
     if (seq_stride < 0 || layer_stride < 0 || head_stride < 0) fail(CLO_ERR_ARGUMENT, "negative stride");
     const int d = cfg_.shape.head_dim;
     const int esz = cfg_.kv_dtype == CLO_DTYPE_BF16 ? 2 : 4;
+    for (int64_t st : {seq_stride, layer_stride, head_stride})
+        if (st * esz % 16 != 0) fail(CLO_ERR_ARGUMENT, "seq/layer/head strides must be multiples of 16 bytes");
     if (row_stride == 0) row_stride = d;
     if (row_stride < d) fail(CLO_ERR_ARGUMENT, "row_stride must be at least head_dim");
     if (row_stride * esz % 16 != 0) fail(CLO_ERR_ARGUMENT, "row_stride must be a multiple of 16 bytes");
@@ -787,7 +793,7 @@ void Engine::prefill(const float* true_q0, int on_host, cudaStream_t user) {
                     const size_t seg = ((size_t)b * L + l) * H + g;
                     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH)
                         segs.push_back({stage_k.p, d_proj_t_.as<double>() + (size_t)lg * d * cfg_.hash_bits,
-                                        d_codes_.as<uint64_t>() + seg * nmax_ * words_});
+                                        d_codes_.as<uint64_t>() + seg * code_stride_});
                     if (persistent_[lg]) {
                         const size_t p = (size_t)b * np_ + pidx_[lg];
                         CLO_CUDA(cudaMemcpyAsync(d_pk_.as<char>() + p * nmax_ * d * esz, stage_k.p,
@@ -997,9 +1003,17 @@ void Engine::launch_step(int mode, const clo_step_io& io, cudaStream_t user) {
         fail(CLO_ERR_ARGUMENT, "step inputs must be non-null");
     CLO_CUDA(cudaSetDevice(cfg_.device));
     const clo_model_shape& s = cfg_.shape;
+    // Steps may be issued on different streams: each one reads the single
+    // device descriptor and mutates shared engine state, so step t+1 waits
+    // for step t's graph wherever it was launched.
+    if (!ev_step_) CLO_CUDA(cudaEventCreateWithFlags(&ev_step_, cudaEventDisableTiming));
+    if (step_stream_set_ && step_stream_ != user) CLO_CUDA(cudaStreamWaitEvent(user, ev_step_, 0));
     set_desc(make_desc(io, user), user);
     if (!execs_[mode]) capture_graph(mode);
     CLO_CUDA(cudaGraphLaunch(execs_[mode], user));
+    CLO_CUDA(cudaEventRecord(ev_step_, user));
+    step_stream_ = user;
+    step_stream_set_ = true;
     launches_ += kernels_per_step_;
     if (pending_free_ >= 0) {  // the staging slot is reusable once this graph is done
         CLO_CUDA(cudaEventRecord(ev_free_[pending_free_], user));
@@ -1164,6 +1178,10 @@ void Engine::check_device_error() {
     if (err & kErrNonFiniteKey) fail(CLO_ERR_NUMERIC, "non-finite key entry");
     if (err & kErrNonFiniteValue) fail(CLO_ERR_NUMERIC, "non-finite value entry");
     if (err & kErrContract) fail(CLO_ERR_CONTRACT, "device-side contract violation");
+    if (err & kErrAlias)
+        fail(CLO_ERR_CONTRACT,
+             "layer_stride 0 aliases one host K/V store across layers, but a step's new K/V rows differ "
+             "between layers");
     if (err & kErrExchange)
         fail(CLO_ERR_CUDA, "head-output exchange timed out: a peer rank stopped stepping");
     fail(CLO_ERR_INTERNAL, "device-side error flag " + std::to_string(err));

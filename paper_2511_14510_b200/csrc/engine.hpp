@@ -86,6 +86,10 @@ class Engine {
     int np_ = 0, no_ = 0;
     int sync_mode_ = CLO_SYNC_GPU_CENTRIC;
     int nmax_ = 0, max_chunks_ = 0, words_ = 0, nb_ = 0, max_attn_chunks_ = 0;
+    int64_t code_stride_ = 0;
+    cudaEvent_t ev_step_ = nullptr;     // recorded after each step's graph (cross-stream step order)
+    cudaStream_t step_stream_ = nullptr;  // stream of the previous step
+    bool step_stream_set_ = false;  // u64 words per segment's codes, even (16-byte aligned segments)
 
     void* host_k_ = nullptr;
     void* host_v_ = nullptr;

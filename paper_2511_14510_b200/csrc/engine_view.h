@@ -15,7 +15,10 @@
 //   entry_slot/slot_tok [B*NO][k]     offloaded: which slot holds the i-th entry
 //                                     token / which token each slot holds (the
 //                                     delta gather keeps surviving rows in place)
-//   codes           [B*L*H][nmax][words] u64 sign-hash bits (RetrievalMetadata::bits)
+//   codes           [B*L*H][code_stride] u64 sign-hash bits (RetrievalMetadata::bits):
+//                   row j of segment s at codes + s*code_stride + j*words;
+//                   code_stride = nmax*words rounded up to an even word count so
+//                   every segment starts 16-byte aligned (TMA bulk copies)
 //   proj_t          [L*H][d][bits] f64  projection transposed (P^T)
 //   labels          [B*L*hq][d] f64, label_valid [B*L*hq]   (QueryLabel)
 //   tau [L*H], qimp [L*H][m]                       (HeadProfileEntry)
@@ -92,6 +95,7 @@ struct EngineView {
     int32_t* entry_slot;   // [B*NO][k] slot holding the i-th (ascending) entry token
     int32_t* slot_tok;     // [B*NO][k] token held by each slot
     uint64_t* codes;
+    int64_t code_stride;   // u64 words per segment (even)
     const double* proj_t;
     double* labels;
     int* label_valid;

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
         else
             it.rows = v.kmirror ? (const char*)v.kmirror + ((size_t)b * v.NO + v.oidx[lg]) * v.nmax * row_bytes
                                 : nullptr;
-        it.codes = v.codes ? v.codes + (size_t)seg * v.nmax * v.words : nullptr;
+        it.codes = v.codes ? v.codes + (size_t)seg * v.code_stride : nullptr;
         // persistent heads select straight into their entry; offloaded heads
         // select into scratch and are reconciled with the old entry (delta gather)
         it.out_idx = pers ? v.entry_idx + (size_t)seg * v.k : a.s.sel + (size_t)item * v.k;

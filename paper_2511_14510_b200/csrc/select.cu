@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
     auto issue = [&](int i) {  // thread 0
         int item, chunk, row0, rows;
         piece(i, item, chunk, row0, rows);
-        const uint32_t bytes = (uint32_t)rows * W * 8 / 16 * 16;
+        const uint64_t* src = a.items[item].codes + (size_t)row0 * W;
+        // cp.async.bulk needs a 16-byte aligned source: a misaligned piece
+        // (caller-provided codes at an odd word offset) is read by LSU loads
+        const uint32_t bytes = (reinterpret_cast<uintptr_t>(src) & 15) ? 0u : (uint32_t)rows * W * 8 / 16 * 16;
         uint64_t* b = &bar[i & 1];
         if (bytes) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                     smem_addr(stage + (size_t)(i & 1) * kPieceRows * W)),
-                "l"(a.items[item].codes + (size_t)row0 * W), "r"(bytes), "r"(smem_addr(b))
+                "l"(src), "r"(bytes), "r"(smem_addr(b))
                 : "memory");
         } else {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
@@ -158,8 +161,9 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
             "r"((i >> 1) & 1)
             : "memory");
         const uint64_t* st = stage + (size_t)(i & 1) * kPieceRows * W;
-        const int copied = rows * W * 8 / 16 * 16 / (W * 8);  // whole rows in smem
         const uint64_t* codes = a.items[item].codes;
+        const bool staged = (reinterpret_cast<uintptr_t>(codes + (size_t)row0 * W) & 15) == 0;
+        const int copied = staged ? rows * W * 8 / 16 * 16 / (W * 8) : 0;  // whole rows in smem
         uint16_t* keys = a.key16 + (size_t)item * a.nmax;
         uint32_t* myhist = whist + warp * a.nb;
 #pragma unroll 4

@@ -29,6 +29,38 @@ def test_hash_widths(oracle, bits):
     run_and_compare(make_case(hash_bits=bits, steps=6), oracle)
 
 
+@pytest.mark.parametrize("bits", [64, 192, 320])
+def test_hash_widths_odd_segment_length(oracle, bits):
+    """Odd code words per row and an odd n_prompt + steps: every other
+    segment's codes would start 8-byte aligned without the engine's even
+    per-segment code stride (the TMA score kernel's bulk copies need 16)."""
+    case = make_case(hash_bits=bits, n_prompt=97, steps=6)
+    assert (97 + 6) % 2 == 1 and case["cfg"].batch * case["cfg"].shape.num_kv_heads >= 2
+    run_and_compare(case, oracle)
+
+
+def test_aliased_host_store_rejects_layer_dependent_rows():
+    """layer_stride 0 aliases one host matrix across layers: a step whose new
+    K/V rows differ between layers is a ContractError, not silent corruption."""
+    from paper_2511_14510_b200._lib import ContractError
+    case = make_case(L=3, steps=3, alias_layers=True)
+    wl = case["wl"]
+    g = gpu_engine(case)
+    g.prefill()
+    g.decode_step()  # identical rows across layers: fine
+    g.metrics()  # synchronises; raises a deferred device error
+    base = wl.step_new_kv
+
+    def skewed(t):
+        k, v = base(t)
+        k = k.copy()
+        k[:, 2] = k[:, 0] + 1.0  # f32 rows: layer 2 appends a different key
+        return k, v
+    wl.step_new_kv = skewed
+    with pytest.raises(ContractError, match="aliases"):
+        g.decode_step()  # synchronises: the device-side check surfaces here
+
+
 def test_tie_heavy_integer_keys_exact(oracle):
     # integer-valued keys and queries: exact dot products collide massively;
     # the (score desc, index asc) order decides every selection
