@@ -264,6 +264,9 @@ def run_ours(args):
     if args.same_device:  # functional multi-rank check on a 1-GPU box (not a bench number)
         local = 0
         os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    elif world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPUs "
+                         "(--same-device runs every rank on cuda:0 as a functional check)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -298,8 +301,23 @@ def run_ours(args):
     gen.manual_seed(args.seed * 1000 + rank)
     t_setup = time.time()
 
+    # NUMA placement: this rank's pinned host shard lives on the
+    # host node of its GPU's PCIe root, and its host threads run there, so the
+    # zero-copy gathers never cross the socket interconnect.
+    from paper_2511_14510_b200.engine import device_numa_node, numa_node_cpus
+    node = device_numa_node(local)
+    multi_node = os.path.exists("/sys/devices/system/node/node1")
+    numa = {"gpu_node": node, "host_nodes": "multi" if multi_node else "single", "bound": False}
+    if node >= 0 and multi_node:
+        cpus = numa_node_cpus(node)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            numa["cpus"] = len(cpus)
+        numa["bound"] = True
+
     # host KV: one aliased [B][1][H][nmax][d] bf16 buffer pair (see module doc)
-    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge, interleaved=args.kv_layout == "interleaved")
+    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge, interleaved=args.kv_layout == "interleaved",
+                 numa_node=node if numa["bound"] else -1)
     for b in range(B):
         for arr in (hkv.k, hkv.v):
             x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -594,7 +612,7 @@ def run_ours(args):
                        "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
                                   + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
                                      else "separate K and V matrices"),
-                       "sigma_step": args.sigma, "sigma_layer": args.sigma_layer},
+                       "sigma_step": args.sigma, "sigma_layer": args.sigma_layer, "numa": numa},
             "hit_ratio": hits / max(1, hits + misses),
             "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms), "max": max(step_ms)},
             "pcie_gather_gbs_in_step": gathered / (ms / 1e3) / 1e9,
@@ -611,8 +629,26 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-run this script
+    under torch.distributed.run with N ranks on this node (one process per
+    GPU, rendezvous on 127.0.0.1), the way the reference's runner fans
+    independent engines out over a worker pool (runner.cpp:186-278). Rank 0
+    prints the JSON line; the launcher's exit code is returned."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

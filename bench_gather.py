@@ -11,9 +11,13 @@ matrix (the engine batches every missed head of a layer the same way).
 Engines: lsu = 16-byte zero-copy loads (the engine's kernel), tma = one
 cp.async.bulk per row from pinned host memory.
 
-  python bench_gather.py [--heads 32] [--reps 5] [--threads 16]
+  python bench_gather.py [--heads 32] [--reps 5] [--threads 16] [--gpus N]
 
-Prints one JSON line per row count, then a summary line.
+Prints one JSON line per row count, then a summary line. With --gpus N, one
+process per GPU runs the same sweep CONCURRENTLY (a barrier before every timed
+repetition), each from its own pinned host store bound to its GPU's NUMA node,
+so PCIe-switch uplink sharing shows up; each line then carries the per-GPU
+rates and their aggregate.
 """
 from __future__ import annotations
 
@@ -30,8 +34,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+class _NoBarrier:
+    def wait(self):
+        pass
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1, help="concurrent per-GPU sweeps (one process per GPU)")
+    ap.add_argument("--same-device", action="store_true", help="testing only: every worker on cuda:0")
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--threads", type=int, default=min(16, os.cpu_count() or 1))
@@ -46,11 +57,69 @@ def main():
     ap.add_argument("--active", type=int, default=0,
                     help="gather from only this many (random) heads of the store (0 = all)")
     args = ap.parse_args()
+    if args.gpus <= 1:
+        results, peak = sweep(0, args, _NoBarrier(), emit=True)
+        summarize([results], [peak], args)
+        return
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    barrier = ctx.Barrier(args.gpus)
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, args, barrier, q)) for r in range(args.gpus)]
+    for p in procs:
+        p.start()
+    got = dict(q.get() for _ in procs)
+    for p in procs:
+        p.join()
+        if p.exitcode:
+            raise SystemExit(f"gather worker exited with {p.exitcode}")
+    per = [got[r][0] for r in range(args.gpus)]
+    peaks = [got[r][1] for r in range(args.gpus)]
+    for i, line in enumerate(per[0]):
+        rows = [p[i] for p in per]
+        agg = {"rows_per_head": line["rows_per_head"], "gpus": args.gpus, "heads_per_gpu": line["heads"],
+               "bytes_per_gpu": line["bytes"], "concurrent": True}
+        for key in ("lsu", "tma", "cpu_staged"):
+            if key + "_gbs" in line:
+                agg[key + "_gbs_per_gpu"] = [round(x[key + "_gbs"], 3) for x in rows]
+                # conservative: every GPU's bytes over the slowest GPU's time
+                agg[key + "_gbs_aggregate"] = sum(x["bytes"] for x in rows) / (max(x[key + "_ms"] for x in rows) * 1e-3) / 1e9
+        agg["link_peak_gbs_per_gpu"] = [round(p, 3) for p in peaks]
+        print(json.dumps(agg), flush=True)
+    summarize(per, peaks, args)
 
+
+def _worker(rank, args, barrier, q):
+    args.threads = max(1, args.threads // args.gpus)
+    results, peak = sweep(rank, args, barrier, emit=False)
+    q.put((rank, (results, peak)))
+
+
+def summarize(per, peaks, args):
+    flat = [x for r in per for x in r]
+    print(json.dumps({"summary": f"zero-copy gather sweep (configs[4]), {args.gpus} GPU(s)"
+                                 + (" concurrently" if args.gpus > 1 else ""),
+                      "link_peak_gbs_pinned_memcpy": peaks if args.gpus > 1 else peaks[0],
+                      "pcie_gen5_x16_theoretical_gbs": 64.0,
+                      "best_lsu_gbs": max(x["lsu_gbs"] for x in flat),
+                      "best_tma_gbs": max(x["tma_gbs"] for x in flat),
+                      "best_lsu_gbs_aggregate": max(sum(r[i]["bytes"] for r in per) / max(r[i]["lsu_ms"] for r in per)
+                                                    / 1e6 for i in range(len(per[0]))),
+                      "best_tma_gbs_aggregate": max(sum(r[i]["bytes"] for r in per) / max(r[i]["tma_ms"] for r in per)
+                                                    / 1e6 for i in range(len(per[0]))),
+                      "best_cpu_staged_gbs": max((x.get("cpu_staged_gbs", 0.0) for x in flat))}),
+          flush=True)
+
+
+def sweep(rank, args, barrier, emit):
     import torch
     from paper_2511_14510_b200 import _lib
+    from paper_2511_14510_b200.engine import device_numa_node
     lib = _lib.load()
-    dev = torch.device("cuda", 0)
+    gpu = 0 if args.same_device else rank
+    dev = torch.device("cuda", gpu)
+    torch.cuda.set_device(dev)
+    node = device_numa_node(gpu) if os.path.exists("/sys/devices/system/node/node1") else -1
     d, esz, n, H = args.d, 2, args.n, args.heads
     row_bytes = d * esz
     # host store: H heads x n rows, K and V, pinned + mapped
@@ -58,7 +127,7 @@ def main():
     ptrs = []
     for _ in range(2):
         p = C.c_void_p()
-        _lib.check(lib.clo_host_alloc_ex(nbytes, _lib.HOST_HUGEPAGES if args.huge else 0, C.byref(p)))
+        _lib.check(lib.clo_host_alloc_numa(nbytes, _lib.HOST_HUGEPAGES if args.huge else 0, node, C.byref(p)))
         ptrs.append(p.value)
         arr = np.frombuffer((C.c_char * nbytes).from_address(p.value), dtype=np.uint16)
         arr[:] = np.random.default_rng(len(ptrs)).integers(0, 65535, arr.size, dtype=np.uint16)
@@ -72,6 +141,7 @@ def main():
     peak = 0.0
     for _ in range(5):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier.wait()  # with --gpus N: every GPU's link under load at once
         a.record(stream)
         dbuf.copy_(pin, non_blocking=True)
         b.record(stream)
@@ -90,17 +160,18 @@ def main():
         moved = 2 * nsel * row_bytes
         line = {"rows_per_head": r, "heads": H, "bytes": moved, "n": n, "hugepages": args.huge}
         if args.kv_one_launch:  # one store [2][H*n] rows: indices into K then V halves, one launch
-            if not hasattr(main, "_kv"):
+            if not hasattr(sweep, "_kv"):
                 p = C.c_void_p()
-                _lib.check(lib.clo_host_alloc(2 * nbytes, C.byref(p)))
-                main._kv = p.value
+                _lib.check(lib.clo_host_alloc_numa(2 * nbytes, 0, node, C.byref(p)))
+                sweep._kv = p.value
             didx2 = torch.cat([didx, didx + H * n])
             dst2 = torch.empty((2 * nsel, d), dtype=torch.int16, device=dev)
             best = None
             for rep in range(args.reps + 1):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                barrier.wait()
                 a.record(stream)
-                _lib.check(lib.clo_gather_rows_ex(main._kv, _lib.DTYPE_BF16, d, 2 * H * n, didx2.data_ptr(), 2 * nsel,
+                _lib.check(lib.clo_gather_rows_ex(sweep._kv, _lib.DTYPE_BF16, d, 2 * H * n, didx2.data_ptr(), 2 * nsel,
                                                   dst2.data_ptr(), 0, args.ctas, err.data_ptr(), sp))
                 b.record(stream)
                 torch.cuda.synchronize()
@@ -112,6 +183,7 @@ def main():
             best = None
             for rep in range(args.reps + 1):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                barrier.wait()
                 a.record(stream)
                 for m in range(2):
                     _lib.check(lib.clo_gather_rows_ex(ptrs[m], _lib.DTYPE_BF16, d, H * n, didx.data_ptr(), nsel,
@@ -134,7 +206,8 @@ def main():
             line["link_peak_gbs"] = peak
             line["lsu_frac_of_peak"] = line["lsu_gbs"] / peak
             results.append(line)
-            print(json.dumps(line), flush=True)
+            if emit:
+                print(json.dumps(line), flush=True)
             continue
         stg = C.c_void_p()
         _lib.check(lib.clo_host_alloc(nsel * row_bytes, C.byref(stg)))
@@ -142,6 +215,7 @@ def main():
         best = None
         for rep in range(min(args.reps, 3) + 1):
             torch.cuda.synchronize()
+            barrier.wait()
             t0 = time.perf_counter()
             for m in range(2):
                 _lib.check(lib.clo_gather_rows_cpu_staged(ptrs[m], _lib.DTYPE_BF16, d, H * n, hidx.ctypes.data, nsel,
@@ -158,15 +232,11 @@ def main():
         line["lsu_frac_of_peak"] = line["lsu_gbs"] / peak
         line["tma_frac_of_peak"] = line["tma_gbs"] / peak
         results.append(line)
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
     for p in ptrs:
         lib.clo_host_free(p)
-    print(json.dumps({"summary": "zero-copy gather sweep (configs[4]), 1 GPU",
-                      "link_peak_gbs_pinned_memcpy": peak, "pcie_gen5_x16_theoretical_gbs": 64.0,
-                      "best_lsu_gbs": max(x["lsu_gbs"] for x in results),
-                      "best_tma_gbs": max(x["tma_gbs"] for x in results),
-                      "best_cpu_staged_gbs": max((x.get("cpu_staged_gbs", 0.0) for x in results))}),
-          flush=True)
+    return results, peak
 
 
 if __name__ == "__main__":

@@ -321,6 +321,15 @@ clo_status clo_host_alloc(size_t bytes, void** out);
  * Freed with clo_host_free. */
 #define CLO_HOST_HUGEPAGES 1
 clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out);
+/* Same, with every page bound (mbind MPOL_BIND, first touch under the policy,
+ * then cudaHostRegister) to host NUMA node `numa_node`: the node of the PCIe
+ * root the GPU that gathers from this store hangs off, so its zero-copy reads
+ * never cross the socket interconnect. numa_node < 0 means
+ * no binding (= clo_host_alloc_ex). Freed with clo_host_free. */
+clo_status clo_host_alloc_numa(size_t bytes, int flags, int numa_node, void** out);
+/* NUMA node of CUDA device `device`'s PCIe root (sysfs numa_node of its PCI
+ * bus id); -1 when the host does not report one (single-node hosts). */
+clo_status clo_device_numa_node(int device, int* node);
 clo_status clo_host_free(void* p);
 clo_status clo_host_register(void* p, size_t bytes);
 clo_status clo_host_unregister(void* p);

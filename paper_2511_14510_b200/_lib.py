@@ -170,6 +170,8 @@ SIGNATURES = {
     "clo_last_error": (C.c_char_p, []),
     "clo_host_alloc": (_I, [C.c_size_t, C.POINTER(_P)]),
     "clo_host_alloc_ex": (_I, [C.c_size_t, _I, C.POINTER(_P)]),
+    "clo_host_alloc_numa": (_I, [C.c_size_t, _I, _I, C.POINTER(_P)]),
+    "clo_device_numa_node": (_I, [_I, C.POINTER(_I)]),
     "clo_host_free": (_I, [_P]),
     "clo_host_register": (_I, [_P, C.c_size_t]),
     "clo_host_unregister": (_I, [_P]),

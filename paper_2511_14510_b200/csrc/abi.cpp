@@ -1,6 +1,12 @@
 // abi.cpp — the C-ABI (include/clo.h): engine entry points, op-level entry
 // points and the host-side pure functions of the path.
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <cerrno>
+#include <cstdio>
 
 #include <algorithm>
 #include <cmath>
@@ -290,19 +296,47 @@ std::mutex g_huge_mu;
 std::unordered_map<void*, size_t> g_huge;
 }  // namespace
 
-clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out) {
+clo_status clo_host_alloc_numa(size_t bytes, int flags, int numa_node, void** out) {
     return guarded([&] {
         require_device();
-        if (!(flags & CLO_HOST_HUGEPAGES)) {
+        if (!(flags & CLO_HOST_HUGEPAGES) && numa_node < 0) {
             CLO_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
             return;
         }
-        const size_t huge = size_t(2) << 20;
-        const size_t len = (bytes + huge - 1) / huge * huge;
+        const size_t page = (flags & CLO_HOST_HUGEPAGES) ? size_t(2) << 20 : size_t(4) << 10;
+        const size_t len = (bytes + page - 1) / page * page;
         void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
         if (p == MAP_FAILED) fail(CLO_ERR_IO, "mmap of the host K/V store failed");
-        madvise(p, len, MADV_HUGEPAGE);
-        std::memset(p, 0, len);  // fault the (huge) pages in before pinning
+        if (flags & CLO_HOST_HUGEPAGES) madvise(p, len, MADV_HUGEPAGE);
+        if (numa_node >= 0) {
+            // mbind(MPOL_BIND) through the raw syscall (no libnuma in the image):
+            // the pages are allocated on `numa_node` when first touched below
+            constexpr int kMaxNodes = 1024;
+            if (numa_node >= kMaxNodes) {
+                munmap(p, len);
+                fail(CLO_ERR_ARGUMENT, "numa_node out of range");
+            }
+            unsigned long mask[kMaxNodes / (8 * sizeof(unsigned long))] = {};
+            mask[numa_node / (8 * sizeof(unsigned long))] |= 1ul << (numa_node % (8 * sizeof(unsigned long)));
+            constexpr int kMpolBind = 2;
+            if (syscall(SYS_mbind, p, len, kMpolBind, mask, (unsigned long)kMaxNodes, 0u) != 0) {
+                munmap(p, len);
+                fail(CLO_ERR_IO, "mbind of the host K/V store to NUMA node " + std::to_string(numa_node) +
+                                     " failed: " + std::strerror(errno));
+            }
+        }
+        // fault the pages in (under the NUMA policy) before pinning, from
+        // several threads: a store of tens of GB takes seconds on one core
+        {
+            const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+            const size_t per = (len / nt + page - 1) / page * page;
+            std::vector<std::thread> th;
+            for (unsigned i = 0; i < nt; ++i) {
+                const size_t a = i * per, b = std::min(len, a + per);
+                if (a < b) th.emplace_back([=] { std::memset(static_cast<char*>(p) + a, 0, b - a); });
+            }
+            for (auto& t : th) t.join();
+        }
         cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
         if (e != cudaSuccess) {
             munmap(p, len);
@@ -314,7 +348,28 @@ clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out) {
     });
 }
 
+clo_status clo_host_alloc_ex(size_t bytes, int flags, void** out) {
+    return clo_host_alloc_numa(bytes, flags, -1, out);
+}
+
 clo_status clo_host_alloc(size_t bytes, void** out) { return clo_host_alloc_ex(bytes, 0, out); }
+
+clo_status clo_device_numa_node(int device, int* node) {
+    return guarded([&] {
+        if (!node) fail(CLO_ERR_ARGUMENT, "node must be non-null");
+        require_device();
+        char bus[32] = {};
+        CLO_CUDA(cudaDeviceGetPCIBusId(bus, sizeof bus, device));
+        for (char* c = bus; *c; ++c) *c = (char)std::tolower((unsigned char)*c);
+        *node = -1;
+        const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+        if (FILE* f = std::fopen(path.c_str(), "r")) {
+            int v = -1;
+            if (std::fscanf(f, "%d", &v) == 1) *node = v;
+            std::fclose(f);
+        }
+    });
+}
 
 clo_status clo_host_free(void* p) {
     return guarded([&] {

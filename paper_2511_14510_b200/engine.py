@@ -136,10 +136,12 @@ class HostKV:
 
     interleaved=True stores one buffer [B][Lk][H][nmax][2][d]: a token's K and
     V rows are contiguous (row stride 2d), so fetching it over PCIe touches one
-    host page instead of two. `k` and `v` are strided views either way."""
+    host page instead of two. `k` and `v` are strided views either way.
+    numa_node >= 0 binds the pages to that host NUMA node (the one the gathering
+    GPU's PCIe root hangs off, `device_numa_node`)."""
 
     def __init__(self, batch, layers, heads, nmax, d, kv_dtype, hugepages: bool = False,
-                 interleaved: bool = False):
+                 interleaved: bool = False, numa_node: int = -1):
         lib = _lib.load()
         self.np_dtype = np.uint16 if kv_dtype == "bf16" else np.float32
         self.shape = (batch, layers, heads, nmax, d)
@@ -150,7 +152,8 @@ class HostKV:
         for _ in range(1 if interleaved else 2):
             p = C.c_void_p()
             size = 2 * nbytes if interleaved else nbytes
-            check(lib.clo_host_alloc_ex(size, _lib.HOST_HUGEPAGES if hugepages else 0, C.byref(p)))
+            # numa_node >= 0: pages bound to the GPU's host NUMA node (clo_host_alloc_numa)
+            check(lib.clo_host_alloc_numa(size, _lib.HOST_HUGEPAGES if hugepages else 0, numa_node, C.byref(p)))
             self._ptrs.append(p.value)
             buf = (C.c_char * size).from_address(p.value)
             arrays.append(np.frombuffer(buf, dtype=self.np_dtype))
@@ -172,6 +175,28 @@ class HostKV:
     def __del__(self):
         if getattr(self, "_ptrs", None):
             self.close()
+
+
+def device_numa_node(device: int) -> int:
+    """Host NUMA node of CUDA device `device`'s PCIe root (-1: not reported)."""
+    lib = _lib.load()
+    node = C.c_int(-1)
+    check(lib.clo_device_numa_node(device, C.byref(node)))
+    return node.value
+
+
+def numa_node_cpus(node: int) -> set:
+    """CPUs of host NUMA node `node` (sysfs cpulist), empty when unknown."""
+    try:
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+    except OSError:
+        return set()
+    cpus = set()
+    for part in filter(None, spec.split(",")):
+        a, _, b = part.partition("-")
+        cpus.update(range(int(a), int(b or a) + 1))
+    return cpus
 
 
 class DecodeEngine:

@@ -283,3 +283,31 @@ def test_topk_attention_golden_and_errors(clo):
     with pytest.raises(_lib.NumericError):
         _lib.check(clo.clo_topk_attention(q2.data_ptr(), 1, dev(Kn).data_ptr(), V4.data_ptr(), _lib.DTYPE_F64, 4,
                                           2, dev(np.array([1], np.int32)).data_ptr(), 1, o2.data_ptr(), None))
+
+
+@pytest.mark.parametrize("huge", [0, 1])
+def test_numa_bound_host_store_gathers_bit_exact(clo, huge):
+    """clo_host_alloc_numa: the store is bound to the GPU's NUMA node (node 0
+    when the host reports none) and pinned; zero-copy gathers from it are
+    bit-exact with both copy engines."""
+    from paper_2511_14510_b200.engine import device_numa_node
+    node = device_numa_node(0)
+    assert node >= -1
+    n, d = 5000, 128
+    nbytes = n * d * 2
+    p = C.c_void_p()
+    _lib.check(clo.clo_host_alloc_numa(nbytes, huge, max(node, 0), C.byref(p)))
+    try:
+        host = np.frombuffer((C.c_char * nbytes).from_address(p.value), dtype=np.uint16).reshape(n, d)
+        host[:] = np.random.default_rng(3).integers(0, 65535, host.shape, dtype=np.uint16)
+        idx = np.sort(np.random.default_rng(4).choice(n, 777, replace=False)).astype(np.int32)
+        err = torch.zeros(1, dtype=torch.int32, device=DEV)
+        for engine in (0, 1):
+            out = torch.empty((len(idx), d), dtype=torch.int16, device=DEV)
+            _lib.check(clo.clo_gather_rows_ex(p.value, _lib.DTYPE_BF16, d, n, dev(idx).data_ptr(), len(idx),
+                                              out.data_ptr(), engine, 0, err.data_ptr(), None))
+            torch.cuda.synchronize()
+            assert int(err.item()) == 0
+            np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), host[idx])
+    finally:
+        _lib.check(clo.clo_host_free(p.value))
