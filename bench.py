@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--kv-layout", default="interleaved", choices=["split", "interleaved"],
                     help="host K/V layout: separate K and V matrices, or one token's K|V rows contiguous")
+    ap.add_argument("--kv-dtype", default="bf16", choices=["bf16", "f32"],
+                    help="storage type of the K/V rows (host store, cache slots, attention operands)")
     ap.add_argument("--huge", action="store_true",
                     help="back the pinned host KV store with 2 MiB pages (GPU TLB reach for large stores)")
     ap.add_argument("--same-device", action="store_true",
@@ -152,6 +154,63 @@ def dist_env():
     return world, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def head_profiles(args, threshold, plan_partition):
+    """Synthetic head profiles and the persistent-head plan of the workload,
+    identical in both arms. threshold(s, eta, p) = compute_threshold
+    (head_profile.cpp:17-25); plan_partition(diff, t_comp_s, pcie_bw,
+    mem_head_bytes, persist_bytes_per_head, hbm_budget_bytes) -> (persistent
+    [L][H], n_p, dropped) (head_profile.cpp:80-154). Returns tau [L][H],
+    q_importance [L][H][m], persistent [L][H] int32 and a one-line plan note."""
+    from paper_2511_14510_b200.workload import Shape, synthetic_profiles
+    C2 = args.cfg
+    L, HQ, H, d, n, k, B = (args.layers, C2["q_heads"], C2["kv_heads"], C2["head_dim"], args.ctx, C2["k"],
+                            args.batch)
+    tau, qimp = synthetic_profiles(Shape(L, HQ, H, d), seed=args.seed, threshold=threshold)
+    persistent = np.zeros((L, H), np.int32)
+    persistent[0] = 1  # layer0_only_plan (engine.cpp:548-555)
+    plan_info = "layer0_only_plan"
+    if C2["plan"] == "partition":
+        # plan_partition over synthetic profiles: difficulty = tau - (s_hat - eps),
+        # eps = 0.05 (compute_difficulty :27-30), s_hat ~ U(0.5, 1) per head; N_p
+        # from a 50 us compute window at the measured-order PCIe bandwidth; HBM
+        # budget 80 GiB for the persistent KV of all `B` sequences.
+        rs = np.random.default_rng(args.seed + 17)
+        s_hat = rs.uniform(0.5, 1.0, (L, H))
+        diff = tau - (s_hat - 0.05)
+        row = 2 * d * 2
+        pers, n_p, nd = plan_partition(diff, 5e-5, 5.0e10, float(2 * k * d * 2), row * (n + 4096) * B,
+                                       80 * (1 << 30))
+        persistent = np.asarray(pers, np.int32)
+        plan_info = f"plan_partition: N_p={n_p}, persistent heads={int(persistent.sum())}/{L * H}, dropped={nd}"
+    return tau, qimp, persistent, plan_info
+
+
+def workload_config(args, plan_info, world):
+    """The `config` object of the JSON line, identical in both arms."""
+    C2 = args.cfg
+    shard_heads = C2["shard"] == "heads" and world > 1
+    return {"workload": C2["name"], "batch_per_gpu": args.batch, "ctx": args.ctx, "layers": args.layers,
+            "k": C2["k"], "plan": plan_info,
+            "parallelism": (f"kv-head-sharded x{world} (+{'fused P2P' if args.allgather == 'fused' else 'NCCL'} "
+                            f"head-output all-gather)" if shard_heads else f"request-sharded x{world}"),
+            "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
+            "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
+                       + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
+                          else "separate K and V matrices"),
+            "kv_dtype": args.kv_dtype, "sigma_step": args.sigma, "sigma_layer": args.sigma_layer}
+
+
 # ------------------------------------------------------------ reference arm
 
 def reference_sample(args, steps: int, warmup: int, threads: int):
@@ -178,25 +237,31 @@ def reference_sample(args, steps: int, warmup: int, threads: int):
         aq[t] = _normalize(q + args.sigma_layer * rng.standard_normal(q.shape)).astype(np.float32)
     nk = bf(rng.standard_normal((steps, 1, 1, d), np.float32)).astype(np.float64)
     nv = bf(rng.standard_normal((steps, 1, 1, d), np.float32)).astype(np.float64)
-    qimp = rng.uniform(0, 1, m)
     c = EngineCfg()
     c.num_layers, c.num_q_heads, c.num_kv_heads, c.head_dim, c.bytes_per_element = 1, m, 1, d, 2
     c.k, c.sink_tokens, c.recent_tokens = C2["k"], 4, 64
     c.always_miss = int(C2["always_miss"])
     c.retriever, c.hash_bits, c.retriever_seed, c.policy = 1, 256, 1, 0
     c.n_prompt, c.steps = n, steps
-    tau = 0.3
     if Reference.available():
         kind, lib = "reference", Reference()
     else:
         kind, lib = "port", None
+    # the same head profiles and plan as our arm; thread w serves the w-th of
+    # `threads` offloaded (layer, kv head) units spread evenly over the model
+    prof_lib = lib or Oracle()
+    tau_all, qimp_all, pers, _ = head_profiles(args, prof_lib.compute_threshold, prof_lib.plan_partition)
+    offl = [(l, g) for l in range(pers.shape[0]) for g in range(pers.shape[1]) if not pers[l, g]]
+    pick = [offl[int(i)] for i in np.linspace(0, len(offl) - 1, threads)] if offl else [(0, 0)] * threads
+    tau = np.array([tau_all[l, g] for l, g in pick])
+    qimp = np.array([qimp_all[l, g] for l, g in pick])
     t0 = time.time()
     if lib is not None:
         sps, pre = lib.bench_units(c, tau, qimp, pk, pv, tq, aq, nk, nv, threads, warmup)
         per_unit = float(np.mean(sps))
     else:  # C restatement, one unit per thread is not exposed: time one unit serially
         o = Oracle()
-        e = o.engine(c, np.array([[tau]]), qimp.reshape(1, 1, m), np.zeros((1, 1), np.int32), pk, pv)
+        e = o.engine(c, tau[:1].reshape(1, 1), qimp[:1].reshape(1, 1, m), np.zeros((1, 1), np.int32), pk, pv)
         e.prefill(tq[0])
         for t in range(1, warmup + 1):
             e.decode_step(tq[t], aq[t], nk[t - 1], nv[t - 1])
@@ -212,12 +277,16 @@ def reference_sample(args, steps: int, warmup: int, threads: int):
     tokens_per_s = args.batch * threads / (units_per_token_step * per_unit)
     sample = (f"{threads} concurrent reference DecodeEngines, each one (sequence, layer, KV head) "
               f"unit at ctx={n}, m={m}, k={C2['k']}, sign-hash, similarity policy"
-              f"{' (always_miss)' if C2['always_miss'] else ''}, "
+              f"{' (always_miss)' if C2['always_miss'] else ''}, head profiles (tau, q_importance) of "
+              f"{threads} offloaded (layer, kv head) pairs of the same synthetic profile as the GPU arm, "
               f"{steps - warmup} timed decode_steps after {warmup} warm-up; {per_unit * 1e3:.1f} ms "
-              f"per unit-step; extrapolated x{units_per_token_step} units per batch step "
-              f"(B={args.batch}, L={args.layers}, H={C2['kv_heads']}); wall {wall:.1f}s")
+              f"per unit-step (mean over threads); wall {wall:.1f}s")
+    extrap = (f"EXTRAPOLATED: tokens/s = B * threads / (units per batch step * mean unit-step time) with "
+              f"{units_per_token_step} units per batch step (B={args.batch}, L={args.layers}, H={C2['kv_heads']}); "
+              f"the full batch step is not run on the CPU (it would take "
+              f"{units_per_token_step * per_unit / threads:.0f} s per step)")
     return {"value": tokens_per_s, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
-            "sec_per_unit_step": per_unit}
+            "extrapolation": extrap, "cpu_model": cpu_model(), "sec_per_unit_step": per_unit}
 
 
 def cpu_threads(args):
@@ -231,6 +300,12 @@ def cpu_threads(args):
         ram = 64 << 30
     per_thread = 4 * args.ctx * args.cfg["head_dim"] * 8 + (1 << 28)
     return max(1, min(threads, int(0.5 * ram // per_thread)))
+
+
+def _plan_info_reference(args):
+    from oracle.bind import Oracle, Reference
+    lib = Reference() if Reference.available() else Oracle()
+    return head_profiles(args, lib.compute_threshold, lib.plan_partition)[3]
 
 
 def run_reference_arm(args):
@@ -247,9 +322,9 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * args.batch / cb["value"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.cfg["name"], "batch": args.batch, "ctx": args.ctx,
-                   "layers": args.layers},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": workload_config(args, _plan_info_reference(args), args.gpus),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "extrapolation",
+                                            "cpu_model")},
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -278,8 +353,6 @@ def run_ours(args):
     from paper_2511_14510_b200 import _lib
     from paper_2511_14510_b200.engine import (DecodeEngine, EngineConfig, HostKV, ModelShape, ModeFlags,
                                               layer0_only_plan, profiles_from_arrays)
-    from paper_2511_14510_b200.workload import synthetic_profiles, Shape
-
     lib = _lib.load()
     C2 = args.cfg
     B, L, HQ_all, H_all, d, n, k = (args.batch, args.layers, C2["q_heads"], C2["kv_heads"],
@@ -316,13 +389,19 @@ def run_ours(args):
         numa["bound"] = True
 
     # host KV: one aliased [B][1][H][nmax][d] bf16 buffer pair (see module doc)
-    hkv = HostKV(B, 1, H, nmax, d, "bf16", hugepages=args.huge, interleaved=args.kv_layout == "interleaved",
+    kvd = args.kv_dtype
+    tdt = torch.bfloat16 if kvd == "bf16" else torch.float32
+    esz = 2 if kvd == "bf16" else 4
+    hkv = HostKV(B, 1, H, nmax, d, kvd, hugepages=args.huge, interleaved=args.kv_layout == "interleaved",
                  numa_node=node if numa["bound"] else -1)
     for b in range(B):
         for arr in (hkv.k, hkv.v):
-            x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+            x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
             for h in range(H):  # contiguous [n][d] block of pinned memory: direct D2H
-                torch.from_numpy(arr[b, 0, h, :n].view(np.int16)).copy_(x[h].view(torch.int16))
+                if kvd == "bf16":
+                    torch.from_numpy(arr[b, 0, h, :n].view(np.int16)).copy_(x[h].view(torch.int16))
+                else:
+                    torch.from_numpy(arr[b, 0, h, :n]).copy_(x[h])
 
     # per-step inputs (device resident): drift-walk queries, layer-invariant new rows
     def norm(x):
@@ -335,8 +414,8 @@ def run_ours(args):
             q = norm(q + args.sigma * torch.randn(q.shape, generator=gen, device=dev))
         tq[t] = q
         aq[t] = norm(q + args.sigma_layer * torch.randn(q.shape, generator=gen, device=dev))
-    nk = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(torch.bfloat16).expand(S, B, L, H, d).contiguous()
-    nv = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(torch.bfloat16).expand(S, B, L, H, d).contiguous()
+    nk = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
+    nv = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
     fused_x = shard_heads and args.allgather == "fused"
     HQo = HQ * world if fused_x else HQ  # out's head extent
     out = torch.empty((B, L, HQo, d), device=dev)
@@ -345,27 +424,16 @@ def run_ours(args):
         v = C.c_double()
         _lib.check(lib.clo_compute_threshold(s, eta, p, C.byref(v)))
         return v.value
-    tau, qimp = synthetic_profiles(Shape(L, HQ_all, H_all, d), seed=args.seed, threshold=thr)
-    persistent = np.zeros((L, H_all), np.int32)
-    persistent[0] = 1  # layer0_only_plan (engine.cpp:548-555)
-    plan_info = "layer0_only_plan"
-    if C2["plan"] == "partition":
-        # plan_partition (head_profile.cpp:80-154) over synthetic profiles:
-        # difficulty = tau - (s_hat - eps), eps = 0.05 (compute_difficulty :27-30),
-        # s_hat ~ U(0.5, 1) per head; N_p from a 50 us compute window at the
-        # measured-order PCIe bandwidth; HBM budget 80 GiB for the persistent KV
-        # of all `B` sequences.
-        rs = np.random.default_rng(args.seed + 17)
-        s_hat = rs.uniform(0.5, 1.0, (L, H_all))
-        diff = tau - (s_hat - 0.05)
-        pers = np.zeros((L, H_all), np.int32)
+
+    def plan_partition(diff, t_comp_s, pcie_bw, mem_head_bytes, persist_bytes, budget):
+        Lp, Hp = diff.shape
+        pers = np.zeros((Lp, Hp), np.int32)
         n_p, nd = C.c_int(), C.c_int()
-        row = 2 * d * 2
-        _lib.check(lib.clo_plan_partition(np.ascontiguousarray(diff).ctypes.data, L, H_all, 5e-5, 5.0e10,
-                                          float(2 * k * d * 2), row * (n + 4096) * B, 80 * (1 << 30),
-                                          pers.ctypes.data, C.byref(n_p), C.byref(nd)))
-        persistent = pers
-        plan_info = f"plan_partition: N_p={n_p.value}, persistent heads={int(pers.sum())}/{L * H_all}, dropped={nd.value}"
+        _lib.check(lib.clo_plan_partition(np.ascontiguousarray(diff).ctypes.data, Lp, Hp, t_comp_s, pcie_bw,
+                                          mem_head_bytes, persist_bytes, budget, pers.ctypes.data, C.byref(n_p),
+                                          C.byref(nd)))
+        return pers, n_p.value, nd.value
+    tau, qimp, persistent, plan_info = head_profiles(args, thr, plan_partition)
     sl = slice(hs.kv0, hs.kv0 + hs.n_kv)
     tau, qimp, persistent = tau[:, sl].copy(), qimp[:, sl].copy(), persistent[:, sl].copy()
 
@@ -373,9 +441,9 @@ def run_ours(args):
         n_prompt, steps, alias_layers = n, S, True
         prompt_k = prompt_v = None
 
-    cfg = EngineConfig(shape=ModelShape(L, HQ, H, d, 2), k=k, sink_tokens=4, recent_tokens=64,
+    cfg = EngineConfig(shape=ModelShape(L, HQ, H, d, esz), k=k, sink_tokens=4, recent_tokens=64,
                        retriever="sign_hash", hash_bits=256, retriever_seed=1, policy="similarity",
-                       mode=ModeFlags(always_miss=C2["always_miss"]), batch=B, kv_dtype="bf16",
+                       mode=ModeFlags(always_miss=C2["always_miss"]), batch=B, kv_dtype=kvd,
                        kv_head_offset=hs.kv0, device=local)
     from paper_2511_14510_b200.engine import PartitionPlan
     plan = PartitionPlan(layers=[[g for g in range(H) if persistent[l, g]] for l in range(L)])
@@ -492,7 +560,7 @@ def run_ours(args):
     if E:
         h_tq = torch.empty((E + W, B, L, HQ, d), pin_memory=True)
         h_aq = torch.empty_like(h_tq, pin_memory=True)
-        h_nk = torch.empty((E + W, B, L, H, d), dtype=torch.bfloat16, pin_memory=True)
+        h_nk = torch.empty((E + W, B, L, H, d), dtype=tdt, pin_memory=True)
         h_nv = torch.empty_like(h_nk, pin_memory=True)
         h_out = torch.empty((B, L, HQo, d), pin_memory=True)
         base = t_idx[0]
@@ -516,7 +584,7 @@ def run_ours(args):
         e1.record(stream)
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
-        h2d = (2 * B * L * HQ * d * 4) + 2 * B * L * H * d * 2
+        h2d = (2 * B * L * HQ * d * 4) + 2 * B * L * H * d * esz
         d2h = B * L * HQo * d * 4
         e2e = {"value": (1 if shard_heads else world) * B * E / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d,
@@ -539,7 +607,7 @@ def run_ours(args):
     peaks, peak_kind = measured_peaks()
     total_prof = sum(e["ms"] for e in per_kernel.values()) or 1.0
     dom = max(per_kernel, key=lambda kk: per_kernel[kk]["ms"]) if per_kernel else None
-    row_b = d * 2
+    row_b = d * esz
     W_ = 68
     attn_bytes_launch = B * H * 2 * (k + W_) * row_b          # K+V rows of k + window per head
     gather_ms = per_kernel.get("gather_zero_copy", {}).get("ms", 0.0)
@@ -553,6 +621,7 @@ def run_ours(args):
     rooflines = {
         "gather_zero_copy": {"bound": "pcie", "achieved": gather_gbs, "peak": best, "unit": "GB/s",
                              "frac": gather_gbs / best if best else None,
+                             "frac_of_gen5_x16_theoretical": gather_gbs / 64.0,
                              "traffic": None, "share": gather_ms / total_prof,
                              "bytes_per_unit": "2*k*d*e per missed (seq,layer,kv head) = 1 MiB"},
         "attention": {"bound": "hbm", "achieved": attn_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -595,28 +664,22 @@ def run_ours(args):
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = reference_sample(args, steps=3, warmup=1, threads=cpu_threads(args))
-        cpu_baseline = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
+        cpu_baseline = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample", "extrapolation",
+                                              "cpu_model")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if shard_heads else "weak", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": C2["name"],
-                       "batch_per_gpu": B, "ctx": n, "layers": L, "k": k, "plan": plan_info,
-                       "parallelism": (f"kv-head-sharded x{world} (+{'fused P2P' if fused_x else 'NCCL'} "
-                                       f"head-output all-gather)" if shard_heads
-                                       else f"request-sharded x{world}"),
-                       "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
-                       "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
-                                  + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
-                                     else "separate K and V matrices"),
-                       "sigma_step": args.sigma, "sigma_layer": args.sigma_layer, "numa": numa},
+            "dtype": kvd, "data": "synthetic",
+            "config": workload_config(args, plan_info, world), "numa": numa,
             "hit_ratio": hits / max(1, hits + misses),
             "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms), "max": max(step_ms)},
             "pcie_gather_gbs_in_step": gathered / (ms / 1e3) / 1e9,
-            "pcie_link_peak_gbs": best,
+            "pcie_link_peak_gbs": best, "pcie_gen5_x16_theoretical_gbs": 64.0,
+            "pcie_in_step_frac": {"of_memcpy_peak": gathered / (ms / 1e3) / 1e9 / best if best else None,
+                                  "of_gen5_x16_theoretical": gathered / (ms / 1e3) / 1e9 / 64.0},
             "per_kernel_ms": {kk: round(v["ms"], 4) for kk, v in sorted(per_kernel.items())},
             "roofline": roof, "rooflines": rooflines, "layer_timing": layer_timing,
             "e2e": e2e, "gpu_launches": launches, "kernels_per_step": eng.kernels_per_step(),

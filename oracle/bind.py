@@ -407,13 +407,19 @@ class Reference(_Common):
 
     def bench_units(self, cfg: EngineCfg, tau, q_importance, prompt_k, prompt_v, true_q,
                     approx_q, new_k, new_v, threads, warmup=0):
+        """`threads` independent engines, each one (layer, kv head) unit; tau
+        [threads] and q_importance [threads][m]: thread w's head profile
+        (scalars / one row are broadcast to every thread)."""
+        tau_ = np.ascontiguousarray(np.broadcast_to(np.asarray(tau, np.float64), (threads,)))
+        m = cfg.num_q_heads
+        qi = np.ascontiguousarray(np.broadcast_to(np.asarray(q_importance, np.float64).reshape(-1, m), (threads, m)))
         arrs = [np.ascontiguousarray(a, np.float64) for a in
-                (q_importance, prompt_k, prompt_v, true_q, approx_q, new_k, new_v)]
-        qi, pk, pv, tq, aq, nk, nv = arrs
+                (prompt_k, prompt_v, true_q, approx_q, new_k, new_v)]
+        pk, pv, tq, aq, nk, nv = arrs
         sps = np.zeros(threads)
         pre = np.zeros(threads)
         self._check(self.lib.ref_bench_units(
-            C.byref(cfg), C.c_double(tau), _p(qi, C.c_double), _p(pk, C.c_double),
+            C.byref(cfg), _p(tau_, C.c_double), _p(qi, C.c_double), _p(pk, C.c_double),
             _p(pv, C.c_double), _p(tq, C.c_double), _p(aq, C.c_double), _p(nk, C.c_double),
             _p(nv, C.c_double), C.c_int(threads), C.c_int(warmup), _p(sps, C.c_double),
             _p(pre, C.c_double)))

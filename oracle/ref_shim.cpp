@@ -354,7 +354,7 @@ int ref_run_engine(const ref_engine_cfg* c, const double* tau, const double* q_i
 // The first `warmup` decode steps are untimed. Returns per-thread mean seconds
 // per timed decode_step in sec_per_step[threads] and the prefill seconds in
 // prefill_seconds[threads].
-int ref_bench_units(const ref_engine_cfg* c, double tau, const double* q_importance,
+int ref_bench_units(const ref_engine_cfg* c, const double* tau, const double* q_importance,
                     const double* prompt_k, const double* prompt_v, const double* true_q,
                     const double* approx_q, const double* new_k, const double* new_v,
                     int threads, int warmup, double* sec_per_step, double* prefill_seconds) {
@@ -369,8 +369,10 @@ int ref_bench_units(const ref_engine_cfg* c, double tau, const double* q_importa
                 ArraySource src(cfg.shape, c->n_prompt, c->steps, prompt_k, prompt_v, true_q,
                                 approx_q, new_k, new_v);
                 HeadProfiles profiles(1, std::vector<HeadProfileEntry>(1));
-                profiles[0][0].q_importance.assign(q_importance, q_importance + c->num_q_heads);
-                profiles[0][0].tau = tau;
+                // thread w serves one (layer, kv head) unit with that head's profile
+                profiles[0][0].q_importance.assign(q_importance + (size_t)w * c->num_q_heads,
+                                                   q_importance + (size_t)(w + 1) * c->num_q_heads);
+                profiles[0][0].tau = tau[w];
                 PartitionPlan plan;
                 plan.layers.resize(1);
                 DecodeEngine engine(cfg, profiles, plan, src);

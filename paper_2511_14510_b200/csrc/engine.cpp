@@ -262,7 +262,11 @@ void Engine::allocate() {
     // [B*NO*k rows][d] bf16, boxes of 64 columns x 16 or 32 rows, 128-byte
     // swizzle (the kernel's stage layout). cuTensorMapEncodeTiled comes from
     // the driver through the runtime's entry-point query (no -lcuda).
-    if (cfg_.kv_dtype == CLO_DTYPE_BF16 && (d == 64 || d == 128) && no_ > 0) {
+    static const bool no_tma_slots = [] {  // CLO_ATTN_NOTMA=1: slot tiles by LDGSTS (experiment switch)
+        const char* e = getenv("CLO_ATTN_NOTMA");
+        return e && atoi(e) == 1;
+    }();
+    if (cfg_.kv_dtype == CLO_DTYPE_BF16 && (d == 64 || d == 128) && no_ > 0 && !no_tma_slots) {
         using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

@@ -140,3 +140,41 @@ def test_cpp_shim_compiles_links_and_runs(tmp_path):
     record_trace(SyntheticWorkload(Shape(2, 4, 2, 8), batch=1, n_prompt=16, steps=2, kv_dtype="f32"), trace)
     r = subprocess.run([str(exe), "gpu" if gpu else "cpu", str(trace)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+
+
+@pytest.mark.gpu
+def test_cpp_shim_decodes_on_gpu_like_the_python_path(tmp_path):
+    """The kvsim-named C++ DecodeEngine (include/clo/kvsim.hpp, engine.hpp:91-139)
+    drives prefill + decode_step on the GPU over a trace, and its
+    cache_state_json equals the Python path's on the same inputs and config."""
+    import json
+    import subprocess
+    import numpy as np
+    from paper_2511_14510_b200 import DecodeEngine, EngineConfig, ModeFlags, ModelShape, PartitionPlan
+    from paper_2511_14510_b200 import profiles_from_arrays
+    from paper_2511_14510_b200.trace import TraceSource, record_trace
+    from paper_2511_14510_b200.workload import Shape, SyntheticWorkload
+    exe = tmp_path / "shim_check"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "shim_check.cpp"), "-L", libdir, "-lclo",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    L, hq, hkv, d, n, steps = 3, 8, 2, 64, 300, 10
+    trace = tmp_path / "t.bin"
+    record_trace(SyntheticWorkload(Shape(L, hq, hkv, d), batch=1, n_prompt=n, steps=steps, kv_dtype="f32",
+                                   sigma_step=0.15, seed=9), trace)
+    out = tmp_path / "shim_state.json"
+    r = subprocess.run([str(exe), "gpu", str(trace), str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    shim_state = json.loads(out.read_text())
+    m = hq // hkv
+    tau = np.array([[0.55 + 0.1 * ((l + g) % 4) for g in range(hkv)] for l in range(L)])
+    qimp = np.broadcast_to(1.0 + np.arange(m), (L, hkv, m)).copy()
+    cfg = EngineConfig(shape=ModelShape(L, hq, hkv, d, 4), k=64, retriever="sign_hash", retriever_seed=5,
+                       policy="similarity", mode=ModeFlags(), batch=1, kv_dtype="f32")
+    eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), PartitionPlan(layers=[list(range(hkv))] + [[]] * (L - 1)),
+                       TraceSource(trace, kv_dtype="f32"))
+    eng.run()
+    py_state = json.loads(eng.cache_state_json())
+    assert shim_state["totals"]["misses"] > 0 and shim_state["totals"]["hits"] > 0
+    assert shim_state == py_state
