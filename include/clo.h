@@ -110,11 +110,17 @@ typedef struct clo_engine_config {
     int kv_dtype;     /* clo_dtype of K/V rows (BF16 or F32) */
     int kv_head_offset; /* first global KV head of this shard (seeds, profiles) */
     int device;       /* CUDA ordinal */
+    int victim_rows;  /* HBM rows per offloaded head kept beyond the entry: rows
+                       * that left the entry stay resident (least recently left
+                       * evicted first), so a token that returns to a later
+                       * selection is not fetched over PCIe again. Entry
+                       * contents are unchanged; only data movement shrinks.
+                       * < 0: auto (2*k); 0: none. */
 } clo_engine_config;
 
 /* Fills the reference defaults (engine.hpp:30-49): sink 4, recent 64,
  * sign-hash off (exact), hash_bits 256, seed 1, similarity policy,
- * sync_override -1, batch 1, kv_dtype BF16. */
+ * sync_override -1, batch 1, kv_dtype BF16, victim_rows -1 (auto). */
 void clo_engine_config_defaults(clo_engine_config* cfg);
 
 typedef struct clo_engine clo_engine;

@@ -79,6 +79,7 @@ struct EngineConfig {
     int kv_dtype = CLO_DTYPE_BF16;
     int kv_head_offset = 0;
     int device = 0;
+    int victim_rows = -1;  // HBM rows kept per offloaded head beyond the entry (-1: auto = 2k)
 
     clo_engine_config to_c(int n_prompt, int max_steps) const {
         clo_engine_config c;
@@ -104,6 +105,7 @@ struct EngineConfig {
         c.kv_dtype = kv_dtype;
         c.kv_head_offset = kv_head_offset;
         c.device = device;
+        c.victim_rows = victim_rows;
         return c;
     }
 };

@@ -85,7 +85,7 @@ class EngineConfigC(C.Structure):
         ("has_tau_override", C.c_int), ("tau_override", C.c_double), ("sync_override", C.c_int),
         ("collect_outputs", C.c_int), ("compute_oracle_error", C.c_int), ("batch", C.c_int),
         ("n_prompt", C.c_int), ("max_steps", C.c_int), ("kv_dtype", C.c_int),
-        ("kv_head_offset", C.c_int), ("device", C.c_int),
+        ("kv_head_offset", C.c_int), ("device", C.c_int), ("victim_rows", C.c_int),
     ]
 
 

@@ -121,6 +121,7 @@ void clo_engine_config_defaults(clo_engine_config* c) {
     c->sync_override = -1;
     c->batch = 1;
     c->kv_dtype = CLO_DTYPE_BF16;
+    c->victim_rows = -1;
 }
 
 const char* clo_last_error(void) { return g_last_error.c_str(); }

@@ -14,6 +14,8 @@ constexpr int kMaxHeadDim = 256;
 constexpr int kScoreChunk = 4096;  // rows per score/compact work unit
 constexpr int kScoreThreads = 256;
 constexpr int kMaxRanks = 8;      // KV-head shards of one model (one NVSwitch node)
+constexpr int kSlotInEntry = 0x7fffffff;  // slot_age of a pool slot whose token is in the entry
+constexpr int kSlotEmpty = -1;            // slot_age of a never-filled pool slot
 
 enum DType : int { kBF16 = 0, kF32 = 1, kF64 = 2 };
 

@@ -110,6 +110,9 @@ Engine::Engine(const clo_engine_config& cfg, const double* tau, const double* q_
         fail(CLO_ERR_CONFIG, "K/V rows must be a multiple of 16 bytes");
     if (cfg.sink_tokens + cfg.recent_tokens > 4096) fail(CLO_ERR_CONFIG, "window too large");
     if (cfg.k > reconcile_max_k()) fail(CLO_ERR_CONFIG, "k above 8192 is not supported");
+    // pool slots age by decode step in 16-bit radix keys (age + 1)
+    if (cfg.max_steps > 65000) fail(CLO_ERR_CONFIG, "max_steps above 65000 is not supported");
+    if (cfg.victim_rows > (1 << 20)) fail(CLO_ERR_CONFIG, "victim_rows above 2^20 is not supported");
 
     const int L = s.num_layers, H = s.num_kv_heads;
     tau_.assign(tau, tau + (size_t)L * H);
@@ -199,13 +202,23 @@ void Engine::allocate() {
     d_pk_.alloc((size_t)B * np_ * nmax_ * d * esz, false);
     d_pv_.alloc((size_t)B * np_ * nmax_ * d * esz, false);
     if (cfg_.retriever == CLO_RETRIEVER_EXACT) d_kmirror_.alloc((size_t)B * no_ * nmax_ * d * esz, false);
-    d_slot_k_.alloc((size_t)B * no_ * k * d * esz);
-    d_slot_v_.alloc((size_t)B * no_ * k * d * esz);
+    // row pool per offloaded head: the entry's k rows + victim rows that left it
+    pool_ = k + (cfg_.victim_rows < 0 ? 2 * k : cfg_.victim_rows);
+    d_slot_k_.alloc((size_t)B * no_ * pool_ * d * esz);
+    d_slot_v_.alloc((size_t)B * no_ * pool_ * d * esz);
     d_win_k_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
     d_win_v_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
     d_entry_idx_.alloc(sizeof(int32_t) * segs * k + 64);  // +64: 16-byte rounded token bulk copies
     d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
-    d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * k + 64);
+    d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * pool_ + 64);
+    d_slot_age_.alloc(sizeof(int32_t) * B * no_ * pool_);
+    d_tok2slot_.alloc(sizeof(int32_t) * B * no_ * (size_t)nmax_);
+    // empty pool: no token in any slot (-1), no slot for any token (-1), ages
+    // kSlotEmpty (-1: oldest)
+    static_assert(kSlotEmpty == -1, "pool ages are initialised by an 0xFF memset");
+    CLO_CUDA(cudaMemset(d_slot_tok_.p, 0xFF, sizeof(int32_t) * B * no_ * pool_));
+    CLO_CUDA(cudaMemset(d_slot_age_.p, 0xFF, sizeof(int32_t) * B * no_ * pool_));
+    CLO_CUDA(cudaMemset(d_tok2slot_.p, 0xFF, sizeof(int32_t) * B * no_ * (size_t)nmax_));
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
         d_codes_.alloc(sizeof(uint64_t) * segs * code_stride_ + 64, false);
         // projections P (retrieval.cpp:73-74), seed mix_seed(retriever_seed, l, g)
@@ -274,13 +287,13 @@ void Engine::allocate() {
         cudaDriverEntryPointQueryResult q{};
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
             auto encode = reinterpret_cast<EncodeFn>(fn);
-            CUtensorMap maps[4];
+            CUtensorMap maps[2];
             bool ok = true;
-            const cuuint64_t rows = (cuuint64_t)B * no_ * k;
-            for (int i = 0; i < 4; ++i) {
+            const cuuint64_t rows = (cuuint64_t)B * no_ * pool_;
+            for (int i = 0; i < 2; ++i) {
                 const cuuint64_t dims[2] = {(cuuint64_t)d, rows};
                 const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-                const cuuint32_t box[2] = {64, i < 2 ? 16u : 32u};
+                const cuuint32_t box[2] = {64, 1};  // one row per box: loaded 4 at a time (tile::gather4)
                 const cuuint32_t estr[2] = {1, 1};
                 ok = ok && encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (i & 1) ? d_slot_v_.p : d_slot_k_.p,
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -434,6 +447,9 @@ EngineView Engine::view() const {
     v.entry_idx = d_entry_idx_.as<int32_t>();
     v.entry_slot = d_entry_slot_.as<int32_t>();
     v.slot_tok = d_slot_tok_.as<int32_t>();
+    v.slot_age = d_slot_age_.as<int32_t>();
+    v.tok2slot = d_tok2slot_.as<int32_t>();
+    v.pool = pool_;
     v.codes = d_codes_.as<uint64_t>();
     v.code_stride = code_stride_;
     v.proj_t = d_proj_t_.as<double>();
@@ -470,8 +486,6 @@ EngineView Engine::view() const {
         const char* tm = d_tmaps_.as<char>();
         v.tmap_k = tm;
         v.tmap_v = tm + sizeof(CUtensorMap);
-        v.tmap_k32 = tm + 2 * sizeof(CUtensorMap);
-        v.tmap_v32 = tm + 3 * sizeof(CUtensorMap);
     }
     v.HQg = world_ * s.num_q_heads;
     v.q0 = rank_ * s.num_q_heads;
@@ -1282,15 +1296,17 @@ void Engine::entry_rows(int b, int l, int g, void* k_rows, void* v_rows) {
     const size_t bytes = (size_t)cfg_.k * s.head_dim * esz;
     const size_t o = (size_t)b * no_ + oidx_[lg];
     // CacheEntry::k_rows/v_rows are in entry (ascending index) order; the
-    // slots hold them permuted (delta gather), entry_slot maps them back.
+    // head's row pool holds them at arbitrary slots, entry_slot maps them back.
     auto slot_of = fetch<int32_t>(d_entry_slot_, cfg_.k, o * cfg_.k);
     const size_t rb = (size_t)s.head_dim * esz;
-    std::vector<char> tmp(bytes);
+    const size_t pool_bytes = (size_t)pool_ * rb;
+    std::vector<char> tmp(pool_bytes);
+    (void)bytes;
     for (int which = 0; which < 2; ++which) {
         void* dst = which ? v_rows : k_rows;
         if (!dst) continue;
         const DevBuf& src = which ? d_slot_v_ : d_slot_k_;
-        CLO_CUDA(cudaMemcpy(tmp.data(), src.as<char>() + o * bytes, bytes, cudaMemcpyDeviceToHost));
+        CLO_CUDA(cudaMemcpy(tmp.data(), src.as<char>() + o * pool_bytes, pool_bytes, cudaMemcpyDeviceToHost));
         for (int i = 0; i < cfg_.k; ++i)
             std::memcpy(static_cast<char*>(dst) + (size_t)i * rb, tmp.data() + (size_t)slot_of[i] * rb, rb);
     }

@@ -8,13 +8,18 @@
 //   pk/pv           [B*NP][nmax][d]   persistent heads' full KV in HBM
 //   kmirror         [B*NO][nmax][d]   exact retriever only: HBM copy of the
 //                                     offloaded heads' K (parity mode)
-//   slot_k/slot_v   [B*NO][k][d]      cache-entry rows (CacheEntry::k_rows/v_rows)
+//   slot_k/slot_v   [B*NO][pool][d]   HBM row pool of each offloaded head: the
+//                                     k rows of CacheEntry::k_rows/v_rows plus up
+//                                     to `victim` rows that left the entry lately
+//                                     (pool = k + victim)
 //   win_k/win_v     [B*NO][sink+recent][d]  SinkRecentBuffer (sink rows, then ring)
 //   entry_idx       [B*L*H][k] int32  offloaded: CacheEntry::indices;
 //                                     persistent: this step's selection
-//   entry_slot/slot_tok [B*NO][k]     offloaded: which slot holds the i-th entry
-//                                     token / which token each slot holds (the
-//                                     delta gather keeps surviving rows in place)
+//   entry_slot      [B*NO][k]         offloaded: pool slot of the i-th entry token
+//   slot_tok/slot_age [B*NO][pool]    token held by each slot (-1 empty) / step it
+//                                     left the entry (kSlotInEntry while in it, -2
+//                                     empty): least recently left is evicted first
+//   tok2slot        [B*NO][nmax]      pool slot holding each token, -1 if none
 //   codes           [B*L*H][code_stride] u64 sign-hash bits (RetrievalMetadata::bits):
 //                   row j of segment s at codes + s*code_stride + j*words;
 //                   code_stride = nmax*words rounded up to an even word count so
@@ -93,7 +98,10 @@ struct EngineView {
     void* win_v;
     int32_t* entry_idx;
     int32_t* entry_slot;   // [B*NO][k] slot holding the i-th (ascending) entry token
-    int32_t* slot_tok;     // [B*NO][k] token held by each slot
+    int32_t* slot_tok;     // [B*NO][pool] token held by each slot (-1: empty)
+    int32_t* slot_age;     // [B*NO][pool] step the slot's token left the entry
+    int32_t* tok2slot;     // [B*NO][nmax] slot of each resident token (-1: not in HBM)
+    int pool;              // slots per offloaded head (k + victim rows)
     uint64_t* codes;
     int64_t code_stride;   // u64 words per segment (even)
     const double* proj_t;
@@ -133,12 +141,11 @@ struct EngineView {
     unsigned* xflag[kMaxRanks];  // rank r's per-layer arrival counters [L]
     unsigned long long xtimeout_ns;  // a peer silent this long is reported lost
     // TMA tensor maps (CUtensorMap, 64-byte aligned, device memory) over the
-    // cache slots [B*NO*k][d] bf16: 128-byte swizzled boxes of 64 columns x
-    // the attention tile rows; null when not built (f32 rows, other d)
-    const void* tmap_k;    // 16-row boxes
+    // row pool [B*NO*pool][d] bf16: 128-byte swizzled boxes of 64 columns x 1
+    // row, loaded 4 arbitrary rows at a time (tile::gather4) in entry order;
+    // null when not built (f32 rows, other d)
+    const void* tmap_k;    // one-row boxes over the pool [B*NO*pool][d]: TMA gather4
     const void* tmap_v;
-    const void* tmap_k32;  // 32-row boxes
-    const void* tmap_v32;
 };
 
 }  // namespace clo

@@ -50,83 +50,159 @@ __device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
     return lo;
 }
 
-// Per thread: a contiguous run of `per` elements; block-wide exclusive scan
-// of the per-thread counts gives each element's rank.
+// Reconcile of one missed head's entry with its new selection over the head's
+// HBM row pool (one CTA per head; kRecThreads threads):
+//   1. the old entry's slots become eviction candidates, aged `t` (now);
+//   2. every new token already resident in the pool (tok2slot) keeps its
+//      slot — whether it was in the old entry or left it at an earlier step;
+//   3. the remaining tokens take the least recently vacated slots (never
+//      filled first, then by the step they left the entry, ties by slot
+//      index): a two-pass 8-bit radix select over the 16-bit keys age + 1;
+//   4. evicted tokens leave tok2slot; the new ones enter it and go on the
+//      fetch list (token ascending, as the selection).
+// The entry's contents are exactly the reference's (update_entry,
+// similarity_cache.cpp:74-87); only which rows cross PCIe changes.
 __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a) {
     using Scan = cub::BlockScan<int, kRecThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_hist[256];
+    __shared__ int s_digit, s_below;
     extern __shared__ int32_t rs[];
     const EngineView& v = a.v;
-    const int k = v.k;
-    int32_t* old_idx = rs;           // [k]
-    int32_t* old_slot = rs + k;      // [k]
-    int32_t* nsel = rs + 2 * k;      // [k]
-    int32_t* freed = rs + 3 * k;     // [k] freed slots in old-entry order
+    const int k = v.k, P = v.pool;
+    int32_t* nsel = rs;            // [k] new selection (ascending)
+    int32_t* need_pos = rs + k;    // [k] entry positions whose token is not resident
+    int32_t* victims = rs + 2 * k; // [k] slots they take (ascending)
     const int count = a.count[a.layer];
+    const int t = a.fresh ? 0 : *v.dev_step + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (k + kRecThreads - 1) / kRecThreads;
     const int r0 = threadIdx.x * per, r1 = min(k, r0 + per);
+    const int pper = (P + kRecThreads - 1) / kRecThreads;
+    const int p0 = threadIdx.x * pper, p1 = min(P, p0 + pper);
+    // smallest-first digit search over s_hist: the digit holding the
+    // `want`-th smallest candidate and the count below it (warp 0)
+    auto pick_digit = [&](int want) {
+        if (warp == 0) {
+            int running = 0, D = -1, below = 0;
+            for (int b0 = 0; b0 < 256 && D < 0; b0 += 32) {
+                const int x = s_hist[b0 + lane];
+                int incl = x;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o2);
+                    if (lane >= o2) incl += y;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, running + incl >= want);
+                if (hit) {
+                    const int first = __ffs(hit) - 1;
+                    below = running + __shfl_sync(0xffffffffu, incl - x, first);
+                    D = b0 + first;
+                }
+                running += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) {
+                s_digit = D;
+                s_below = below;
+            }
+        }
+        __syncthreads();
+    };
     for (int item = blockIdx.x; item < count; item += gridDim.x) {
         const int seg = a.items[item].seg;
         const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
         const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
         int32_t* e_idx = v.entry_idx + (size_t)seg * k;
         int32_t* e_slot = v.entry_slot + o * k;
-        int32_t* s_tok = v.slot_tok + o * k;
+        int32_t* s_tok = v.slot_tok + o * P;
+        int32_t* s_age = v.slot_age + o * P;
+        int32_t* t2s = v.tok2slot + o * v.nmax;
         const int32_t* sel = a.sel + (size_t)item * k;
         for (int i = threadIdx.x; i < k; i += blockDim.x) {
             nsel[i] = sel[i];
-            old_idx[i] = a.fresh ? -1 : e_idx[i];
-            old_slot[i] = a.fresh ? i : e_slot[i];
+            if (!a.fresh) s_age[e_slot[i]] = t;  // 1) the old entry's rows become candidates
         }
         __syncthreads();
-        // 1) old tokens leaving the entry free their slots (old order)
-        int nfree = 0;
-        if (a.fresh) {
-            nfree = r1 - r0;
-        } else {
-            for (int j = r0; j < r1; ++j) {
-                const int p = lower_bound(nsel, k, old_idx[j]);
-                nfree += !(p < k && nsel[p] == old_idx[j]);
-            }
-        }
-        int fbase;
-        Scan(scan_tmp).ExclusiveSum(nfree, fbase);
-        __syncthreads();
-        for (int j = r0; j < r1; ++j) {
-            bool gone = true;
-            if (!a.fresh) {
-                const int p = lower_bound(nsel, k, old_idx[j]);
-                gone = !(p < k && nsel[p] == old_idx[j]);
-            }
-            if (gone) freed[fbase++] = old_slot[j];
-        }
-        __syncthreads();
-        // 2) new tokens: keep their slot if already resident, else take the
-        //    next freed slot and go on the fetch list
-        int nfetch = 0;
+        // 2) resident tokens keep their slot
+        int nneed = 0;
         for (int i = r0; i < r1; ++i) {
-            const int p = a.fresh ? k : lower_bound(old_idx, k, nsel[i]);
-            nfetch += !(p < k && old_idx[p] == nsel[i]);
+            const int s = t2s[nsel[i]];
+            if (s >= 0) {
+                s_age[s] = kSlotInEntry;
+                e_slot[i] = s;
+            } else {
+                ++nneed;
+            }
         }
-        int base, total;
-        Scan(scan_tmp).ExclusiveSum(nfetch, base, total);
+        int nbase, total;
+        Scan(scan_tmp).ExclusiveSum(nneed, nbase, total);
+        for (int i = r0; i < r1; ++i)
+            if (t2s[nsel[i]] < 0) need_pos[nbase++] = i;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
+        __syncthreads();
+        // 3) the `total` least recently vacated slots: key = age + 1 (empty -1 -> 0)
+        int T = 0, need_eq = 0;
+        if (total > 0) {
+            for (int p = p0; p < p1; ++p) {
+                const int ag = s_age[p];
+                if (ag != kSlotInEntry) atomicAdd(&s_hist[(ag + 1) >> 8], 1);
+            }
+            __syncthreads();
+            pick_digit(total);
+            const int D1 = s_digit, below1 = s_below;
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
+            __syncthreads();
+            for (int p = p0; p < p1; ++p) {
+                const int ag = s_age[p];
+                if (ag != kSlotInEntry && ((ag + 1) >> 8) == D1) atomicAdd(&s_hist[(ag + 1) & 255], 1);
+            }
+            __syncthreads();
+            pick_digit(total - below1);
+            T = (D1 << 8) | s_digit;
+            need_eq = total - below1 - s_below;
+        }
+        int lt = 0, eq = 0;
+        if (total > 0)
+            for (int p = p0; p < p1; ++p) {
+                const int ag = s_age[p];
+                if (ag == kSlotInEntry) continue;
+                lt += ag + 1 < T;
+                eq += ag + 1 == T;
+            }
+        int lt_base, eq_base;
+        Scan(scan_tmp).ExclusiveSum(lt, lt_base);
+        __syncthreads();
+        Scan(scan_tmp).ExclusiveSum(eq, eq_base);
+        if (total > 0) {
+            int pos = lt_base + min(eq_base, need_eq), eq_seen = eq_base;
+            for (int p = p0; p < p1; ++p) {
+                const int ag = s_age[p];
+                if (ag == kSlotInEntry) continue;
+                const int key = ag + 1;
+                if (key < T) {
+                    victims[pos++] = p;
+                } else if (key == T) {
+                    if (eq_seen < need_eq) victims[pos++] = p;
+                    ++eq_seen;
+                }
+            }
+        }
+        __syncthreads();
+        // 4) evict, insert, publish the fetch list (token ascending)
         int32_t* ftok = a.fetch_tok + ((size_t)a.layer * a.items_cap + item) * k;
         int32_t* fslot = a.fetch_slot + ((size_t)a.layer * a.items_cap + item) * k;
-        for (int i = r0; i < r1; ++i) {
-            const int p = a.fresh ? k : lower_bound(old_idx, k, nsel[i]);
-            int slot;
-            if (p < k && old_idx[p] == nsel[i]) {
-                slot = old_slot[p];
-            } else {
-                slot = freed[base];
-                ftok[base] = nsel[i];
-                fslot[base] = slot;
-                ++base;
-                s_tok[slot] = nsel[i];
-            }
-            e_slot[i] = slot;
-            e_idx[i] = nsel[i];
+        for (int j = threadIdx.x; j < total; j += blockDim.x) {
+            const int vs = victims[j], pos = need_pos[j], tok = nsel[pos];
+            const int old = s_tok[vs];
+            if (old >= 0) t2s[old] = -1;  // old is not in the new selection (its slot was a candidate)
+            t2s[tok] = vs;
+            s_tok[vs] = tok;
+            s_age[vs] = kSlotInEntry;
+            e_slot[pos] = vs;
+            ftok[j] = tok;
+            fslot[j] = vs;
         }
+        for (int i = threadIdx.x; i < k; i += blockDim.x) e_idx[i] = nsel[i];
         if (threadIdx.x == 0) a.fetch_count[(size_t)a.layer * a.items_cap + item] = total;
         __syncthreads();
     }
@@ -162,8 +238,8 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
         const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
         const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
         const uint4* src = reinterpret_cast<const uint4*>((const char*)v.host_k + base * dtype_size(v.kv_dtype));
-        uint4* dk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.k * row_bytes);
-        uint4* dv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.k * row_bytes);
+        uint4* dk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.pool * row_bytes);
+        uint4* dv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * row_bytes);
         const int32_t* ftok = a.fetch_tok + li * v.k;
         const int32_t* fslot = a.fetch_slot + li * v.k;
         uint4 r[kUnitUnroll];
@@ -200,7 +276,7 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
     const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
     const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
-    uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.k * row_bytes);
+    uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
     const int32_t* ftok = a.fetch_tok + li * v.k;
     const int32_t* fslot = a.fetch_slot + li * v.k;
     uint4 r[kUnitUnroll];
@@ -250,7 +326,7 @@ __global__ void __launch_bounds__(T) gather_lite_kernel(const __grid_constant__ 
         const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
         const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
         const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
-        uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.k * row_bytes);
+        uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
         const int32_t* ftok = a.fetch_tok + li * v.k;
         const int32_t* fslot = a.fetch_slot + li * v.k;
         uint4 r[U];
@@ -496,8 +572,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
             const int r = grp * kTmaRows + lane;
             src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.row_stride) * dtype_size(v.kv_dtype);
-            dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
-            if (fused) dst2 = (char*)v.slot_v + (o * v.k + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
+            dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.pool + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
+            if (fused) dst2 = (char*)v.slot_v + (o * v.pool + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
         }
     };
     auto load = [&](int i) {
@@ -571,7 +647,7 @@ void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int ro
 }
 
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
-    const size_t sm = sizeof(int32_t) * 4 * (size_t)a.v.k;
+    const size_t sm = sizeof(int32_t) * 3 * (size_t)a.v.k;
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(reconcile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int grid = a.items_cap < 1024 ? a.items_cap : 1024;

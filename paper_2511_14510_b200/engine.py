@@ -71,6 +71,7 @@ class EngineConfig:  # engine.hpp:30-49 (+ B200 fields)
     kv_dtype: str = "bf16"
     kv_head_offset: int = 0
     device: int = 0
+    victim_rows: int = -1  # HBM rows kept per offloaded head beyond the entry (-1: auto = 2k, 0: none)
 
     def to_c(self, n_prompt: int, max_steps: int) -> _lib.EngineConfigC:
         c = _lib.EngineConfigC()
@@ -92,6 +93,7 @@ class EngineConfig:  # engine.hpp:30-49 (+ B200 fields)
         c.collect_outputs, c.compute_oracle_error = int(self.collect_outputs), int(self.compute_oracle_error)
         c.batch, c.n_prompt, c.max_steps = self.batch, n_prompt, max_steps
         c.kv_dtype, c.kv_head_offset, c.device = KvDtype[self.kv_dtype], self.kv_head_offset, self.device
+        c.victim_rows = self.victim_rows
         return c
 
 

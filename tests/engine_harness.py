@@ -16,7 +16,7 @@ POLICY_CODE = {"similarity": 0, "prefetch_only": 3}
 def make_case(L=3, hq=4, hkv=2, d=16, n_prompt=96, steps=12, k=8, batch=2, kv_dtype="f32",
               retriever="sign_hash", policy="similarity", sink=2, recent=8, always_miss=False,
               always_hit=False, tau_override=None, persistent=None, seed=5, sigma_step=0.15,
-              hash_bits=256, alias_layers=False, tau=None, interleaved=False):
+              hash_bits=256, alias_layers=False, tau=None, interleaved=False, victim_rows=-1):
     shape = Shape(L, hq, hkv, d)
     wl = SyntheticWorkload(shape, batch, n_prompt, steps, kv_dtype=kv_dtype, sigma_step=sigma_step,
                            seed=seed, alias_layers=alias_layers)
@@ -33,7 +33,7 @@ def make_case(L=3, hq=4, hkv=2, d=16, n_prompt=96, steps=12, k=8, batch=2, kv_dt
                        sink_tokens=sink, recent_tokens=recent, retriever=retriever,
                        hash_bits=hash_bits, retriever_seed=11, policy=policy,
                        mode=ModeFlags(always_miss, always_hit, tau_override), collect_outputs=True,
-                       batch=batch, kv_dtype=kv_dtype)
+                       batch=batch, kv_dtype=kv_dtype, victim_rows=victim_rows)
     plan = PartitionPlan(layers=[[g for g in range(hkv) if persistent[l, g]] for l in range(L)])
     return dict(shape=shape, wl=wl, cfg=cfg, plan=plan, tau=tau, qimp=qimp,
                 persistent=np.asarray(persistent, np.int32), interleaved=interleaved)
@@ -85,6 +85,49 @@ def rel_l2(got, want):
     return np.where(den > 0, num / np.where(den > 0, den, 1), num)
 
 
+class PoolModel:
+    """The engine's HBM row pool of one offloaded head (gather.cu reconcile):
+    pool = k + victim rows; tokens already resident keep their slot, the rest
+    take the least recently vacated slots (empty first, then by the step
+    their token left the entry, ties by slot index). Returns how many rows
+    each reconcile fetches over PCIe."""
+    IN_ENTRY = 1 << 31
+
+    def __init__(self, k, victim):
+        self.P = k + (2 * k if victim < 0 else victim)
+        self.slot_tok = [-1] * self.P
+        self.age = [-1] * self.P
+        self.t2s = {}
+        self.e_slot = []
+
+    def reconcile(self, new_sel, t, fresh=False):
+        if not fresh:
+            for sl in self.e_slot:
+                self.age[sl] = t
+        e_new = [None] * len(new_sel)
+        need = []
+        for i, tok in enumerate(new_sel):
+            sl = self.t2s.get(int(tok))
+            if sl is None:
+                need.append(i)
+            else:
+                self.age[sl] = self.IN_ENTRY
+                e_new[i] = sl
+        cands = sorted((self.age[p] + 1, p) for p in range(self.P) if self.age[p] != self.IN_ENTRY)
+        victims = sorted(p for _, p in cands[:len(need)])
+        for vs, pos in zip(victims, need):
+            tok = int(new_sel[pos])
+            old = self.slot_tok[vs]
+            if old >= 0:
+                del self.t2s[old]
+            self.t2s[tok] = vs
+            self.slot_tok[vs] = tok
+            self.age[vs] = self.IN_ENTRY
+            e_new[pos] = vs
+        self.e_slot = e_new
+        return len(need)
+
+
 def run_and_compare(case, oracle, check_rows=True, tol=None):
     """Steps both engines in lockstep; asserts bit-exact selections, decisions,
     histories and gathered rows, and outputs within `tol` relative L2."""
@@ -99,14 +142,16 @@ def run_and_compare(case, oracle, check_rows=True, tol=None):
     for e, tq, *_ in o_engs:
         e.prefill(tq[0])
     worst = 0.0
-    fetched_rows = 0  # rows the delta gather must move over PCIe (new \ old entry)
-    prev = {}
+    fetched_rows = 0  # rows the pooled delta gather moves over PCIe (not resident in the head's HBM pool)
+    prev, pools = {}, {}
     for b in range(len(o_engs)):
         for l in range(L):
             for g in range(H):
                 st0 = o_engs[b][0].head_state(l, g)
                 if not st0["persistent"]:
                     prev[(b, l, g)] = (st0["misses"], set(map(int, st0["entry_indices"])))
+                    pools[(b, l, g)] = PoolModel(cfg.k, cfg.victim_rows)
+                    pools[(b, l, g)].reconcile(list(map(int, st0["entry_indices"])), 0, fresh=True)
     for t in range(1, wl.steps + 1):
         out = g_eng.decode_step()
         for b, (e, tq, aq, nk, nv) in enumerate(o_engs):
@@ -125,7 +170,7 @@ def run_and_compare(case, oracle, check_rows=True, tol=None):
                         pm, pset = prev[(b, l, g)]
                         cur = set(map(int, os_["entry_indices"]))
                         if os_["misses"] > pm and cfg.policy == "similarity":
-                            fetched_rows += len(cur - pset)
+                            fetched_rows += pools[(b, l, g)].reconcile(list(map(int, os_["entry_indices"])), t)
                         prev[(b, l, g)] = (os_["misses"], cur)
                         assert gs["window_held_tokens"] == os_["window_held_tokens"], where
                         if cfg.policy == "similarity":

@@ -61,6 +61,19 @@ def test_aliased_host_store_rejects_layer_dependent_rows():
         g.decode_step()  # synchronises: the device-side check surfaces here
 
 
+@pytest.mark.parametrize("victim", [0, 3, 8, 40, -1])
+@pytest.mark.parametrize("interleaved", [False, True])
+def test_row_pool_sizes(oracle, victim, interleaved):
+    """The HBM row pool (entry + victim rows, least recently vacated evicted
+    first): entries and gathered rows stay bit-exact for every pool size, and
+    the PCIe rows moved equal the pool model's count (engine_harness.PoolModel)
+    — from none kept (victim 0: the plain delta gather) to more than the
+    working set."""
+    case = make_case(steps=24, k=8, sigma_step=0.35, victim_rows=victim, interleaved=interleaved,
+                     tau=0.9, kv_dtype="bf16", d=64)
+    run_and_compare(case, oracle)
+
+
 def test_tie_heavy_integer_keys_exact(oracle):
     # integer-valued keys and queries: exact dot products collide massively;
     # the (score desc, index asc) order decides every selection
