@@ -81,6 +81,8 @@ def parse():
                     help="host K/V layout: separate K and V matrices, or one token's K|V rows contiguous")
     ap.add_argument("--kv-dtype", default="bf16", choices=["bf16", "f32"],
                     help="storage type of the K/V rows (host store, cache slots, attention operands)")
+    ap.add_argument("--victim-rows", type=int, default=-1,
+                    help="HBM rows kept per offloaded head beyond its entry (-1: engine default 8k, 0: none)")
     ap.add_argument("--huge", action="store_true",
                     help="back the pinned host KV store with 2 MiB pages (GPU TLB reach for large stores)")
     ap.add_argument("--same-device", action="store_true",
@@ -208,7 +210,8 @@ def workload_config(args, plan_info, world):
             "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
                        + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
                           else "separate K and V matrices"),
-            "kv_dtype": args.kv_dtype, "sigma_step": args.sigma, "sigma_layer": args.sigma_layer}
+            "kv_dtype": args.kv_dtype, "sigma_step": args.sigma, "sigma_layer": args.sigma_layer,
+            "victim_rows": args.victim_rows if args.victim_rows >= 0 else "auto (8k, HBM-capped)"}
 
 
 # ------------------------------------------------------------ reference arm
@@ -444,7 +447,7 @@ def run_ours(args):
     cfg = EngineConfig(shape=ModelShape(L, HQ, H, d, esz), k=k, sink_tokens=4, recent_tokens=64,
                        retriever="sign_hash", hash_bits=256, retriever_seed=1, policy="similarity",
                        mode=ModeFlags(always_miss=C2["always_miss"]), batch=B, kv_dtype=kvd,
-                       kv_head_offset=hs.kv0, device=local)
+                       kv_head_offset=hs.kv0, device=local, victim_rows=args.victim_rows)
     from paper_2511_14510_b200.engine import PartitionPlan
     plan = PartitionPlan(layers=[[g for g in range(H) if persistent[l, g]] for l in range(L)])
     eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), plan, _Src, host_kv=hkv)

@@ -115,7 +115,7 @@ typedef struct clo_engine_config {
                        * evicted first), so a token that returns to a later
                        * selection is not fetched over PCIe again. Entry
                        * contents are unchanged; only data movement shrinks.
-                       * < 0: auto (2*k); 0: none. */
+                       * < 0: auto (8*k, capped at 40% of the free HBM); 0: none. */
 } clo_engine_config;
 
 /* Fills the reference defaults (engine.hpp:30-49): sink 4, recent 64,

@@ -79,7 +79,7 @@ struct EngineConfig {
     int kv_dtype = CLO_DTYPE_BF16;
     int kv_head_offset = 0;
     int device = 0;
-    int victim_rows = -1;  // HBM rows kept per offloaded head beyond the entry (-1: auto = 2k)
+    int victim_rows = -1;  // HBM rows kept per offloaded head beyond the entry (-1: auto = 8k, HBM-capped)
 
     clo_engine_config to_c(int n_prompt, int max_steps) const {
         clo_engine_config c;

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
     if (badq) raise_err(v.err, kErrNonFiniteQuery);
 
     const int32_t* idx = v.entry_idx + (size_t)seg * v.k;
-    const int32_t* eslot = pers ? nullptr : v.entry_slot + (size_t)((size_t)b * v.NO + v.oidx[lg]) * v.k;
+    const int32_t* stok = pers ? nullptr : v.slot_tok + (size_t)((size_t)b * v.NO + v.oidx[lg]) * v.pool;
     const int wrows = v.sink + v.recent;
     const size_t pslot = pers ? (size_t)b * v.NP + v.pidx[lg] : 0;
     const size_t oslot = pers ? 0 : (size_t)b * v.NO + v.oidx[lg];
@@ -120,11 +120,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_engine_kernel(EngineView v,
             if (ok[u]) {
                 if (pos < v.k) {
                     // persistent: the selection indexes the full HBM KV;
-                    // offloaded: the entry's pool slot holds the row
-                    tok = idx[pos];
-                    const size_t row = pers ? (size_t)tok : (size_t)eslot[pos];
-                    kr = (pers ? pk : sk) + row * D;
-                    vr = (pers ? pv : sv) + row * D;
+                    // offloaded: walk the cache slots (delta-gather layout)
+                    tok = pers ? idx[pos] : stok[pos];
+                    kr = pers ? pk + (size_t)tok * D : sk + (size_t)pos * D;
+                    vr = pers ? pv + (size_t)tok * D : sv + (size_t)pos * D;
                 } else {
                     const int w = pos - v.k;
                     tok = w < s1 ? w : wstart + (w - s1);

@@ -336,37 +336,28 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
             const int s = i % kStagesM;
             const uint32_t st = smem_u32(ring + (size_t)s * kStageBytes);
             const int32_t* idx = v.entry_idx + (size_t)seg * v.k;
-            if (lane < sel_rows) cp_async4(smem_u32(&toks[warp][s][lane]), idx + tp + lane);
+            if (lane < sel_rows)
+                cp_async4(smem_u32(&toks[warp][s][lane]), (pers ? idx : v.slot_tok + oslot * v.pool) + tp + lane);
             const int ch = lane % CPR, r0 = lane / CPR;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our ldmatrix reads of the stage
             __syncwarp();
             if (!pers && tp + kTileM <= v.k && v.tmap_k) {
-                // a whole tile of entry rows, scattered over the head's row
-                // pool: TMA tile::gather4 loads 4 pool rows (by index) x 64
-                // columns per op straight into the 128-byte-swizzled stage
-                const int prow = lane < kTileM ? (int)(oslot * v.pool) + v.entry_slot[oslot * v.k + tp + lane] : 0;
-                uint64_t* bar = &full[warp][s];
-                if (lane == 0)
+                // a run of contiguous cache slots: one 2D TMA box per matrix half
+                if (lane == 0) {
+                    uint64_t* bar = &full[warp][s];
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                                  "r"(kStageBytes)
                                  : "memory");
+                    const int row0 = (int)(oslot * v.pool + tp);
 #pragma unroll
-                for (int q = 0; q < kTileM / 4; ++q) {
-                    const int a0 = __shfl_sync(0xffffffffu, prow, 4 * q), a1 = __shfl_sync(0xffffffffu, prow, 4 * q + 1);
-                    const int a2 = __shfl_sync(0xffffffffu, prow, 4 * q + 2), a3 = __shfl_sync(0xffffffffu, prow, 4 * q + 3);
-                    if (lane == 0) {
+                    for (int m2 = 0; m2 < 2; ++m2)
 #pragma unroll
-                        for (int m2 = 0; m2 < 2; ++m2)
-#pragma unroll
-                            for (int hh = 0; hh < D / 64; ++hh)
-                                asm volatile(
-                                    "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::"
-                                    "bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
-                                        st + m2 * kMatBytes + hh * kTileM * 128 + q * 512),
-                                    "l"(m2 ? v.tmap_v : v.tmap_k), "r"(hh * 64), "r"(a0), "r"(a1), "r"(a2), "r"(a3),
-                                    "r"(smem_u32(bar))
-                                    : "memory");
-                    }
+                        for (int hh = 0; hh < D / 64; ++hh)
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%2, %3}], [%4];" ::"r"(st + m2 * kMatBytes + hh * kTileM * 128),
+                                "l"(m2 ? v.tmap_v : v.tmap_k), "r"(hh * 64), "r"(row0), "r"(smem_u32(bar))
+                                : "memory");
                 }
             } else {
                 const size_t pslot = pers ? (size_t)b * v.NP + v.pidx[lg] : 0;
@@ -385,10 +376,9 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
                             const int tok = idx[pos];
                             kr = pk + (size_t)tok * D;
                             vr = pv + (size_t)tok * D;
-                        } else {  // the entry's pool slot holds the row
-                            const int slot = v.entry_slot[oslot * v.k + pos];
-                            kr = sk + (size_t)slot * D;
-                            vr = sv + (size_t)slot * D;
+                        } else {
+                            kr = sk + (size_t)pos * D;
+                            vr = sv + (size_t)pos * D;
                         }
                     } else {
                         const int w = pos - v.k;
@@ -747,7 +737,12 @@ void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
     // capture, so the host call is not on the replay path
     cudaFuncSetAttribute(attn_mma_stream_kernel<D, M, W, S, C, TM, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(v, layer, pl, v.attn_part);
+    EngineView vv = v;
+    if (TM == 32) {  // the tensor maps whose boxes match the tile
+        vv.tmap_k = v.tmap_k32;
+        vv.tmap_v = v.tmap_v32;
+    }
+    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(vv, layer, pl, v.attn_part);
 }
 
 // Register cap: CLO_ATTN_REGCAP=184 lets an 8-warp CTA share its SM with a

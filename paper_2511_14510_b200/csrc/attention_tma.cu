@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 4) attn_tma_kernel(EngineView v, int
     const int32_t* idx = v.entry_idx + (size_t)seg * v.k;
     const size_t pslot = pers ? (size_t)b * v.NP + v.pidx[lg] : 0;
     const size_t oslot = pers ? 0 : (size_t)b * v.NO + v.oidx[lg];
-    const int32_t* eslot = pers ? nullptr : v.entry_slot + oslot * v.k;
+    const int32_t* stok = pers ? nullptr : v.slot_tok + oslot * v.pool;
     const int wrows = v.sink + v.recent;
     const T* pk = static_cast<const T*>(v.pk) + pslot * v.nmax * D;
     const T* pv = static_cast<const T*>(v.pv) + pslot * v.nmax * D;
@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(kThreads, 4) attn_tma_kernel(EngineView v, int
                 const int tok = idx[pos];
                 kr = pk + (size_t)tok * D;
                 vr = pv + (size_t)tok * D;
-            } else {  // the entry's pool slot holds the row
-                kr = sk + (size_t)eslot[pos] * D;
-                vr = sv + (size_t)eslot[pos] * D;
+            } else {
+                kr = sk + (size_t)pos * D;
+                vr = sv + (size_t)pos * D;
             }
         } else {
             const int w = pos - v.k;
@@ -237,10 +237,15 @@ __global__ void __launch_bounds__(kThreads, 4) attn_tma_kernel(EngineView v, int
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&full[s], 2u * rows * kRowBytes + tok_bytes);
-            if (tok_bytes) bulk_g2s(toks[s], idx + tp, tok_bytes, &full[s]);
+            if (tok_bytes) bulk_g2s(toks[s], (pers ? idx : stok) + tp, tok_bytes, &full[s]);
         }
         __syncwarp();
-        if (lane < rows) {  // scattered rows (pool slots, persistent KV, window): one bulk copy per row
+        if (!pers && tp + rows <= v.k) {  // contiguous cache slots: two bulk copies
+            if (lane == 0) {
+                bulk_g2s(kdst, sk + (size_t)tp * D, rows * kRowBytes, &full[s]);
+                bulk_g2s(vdst, sv + (size_t)tp * D, rows * kRowBytes, &full[s]);
+            }
+        } else if (lane < rows) {  // scattered rows: one bulk copy per row
             const T* kr;
             const T* vr;
             rows_of(tp + lane, kr, vr);

@@ -203,7 +203,20 @@ void Engine::allocate() {
     d_pv_.alloc((size_t)B * np_ * nmax_ * d * esz, false);
     if (cfg_.retriever == CLO_RETRIEVER_EXACT) d_kmirror_.alloc((size_t)B * no_ * nmax_ * d * esz, false);
     // row pool per offloaded head: the entry's k rows + victim rows that left it
-    pool_ = k + (cfg_.victim_rows < 0 ? 2 * k : cfg_.victim_rows);
+    // auto (victim_rows < 0): 8k rows per head (profiles/README.md: the PCIe
+    // bytes saved grow with the area up to ~8k at 128K contexts), shrunk so
+    // the victim areas take at most 40% of the HBM still free here
+    int victim = cfg_.victim_rows;
+    if (victim < 0) {
+        victim = 8 * k;
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && B * no_ > 0) {
+            const size_t per_row = 2 * (size_t)d * esz;  // K + V
+            const size_t fit = (size_t)(0.4 * (double)free_b) / ((size_t)B * no_ * per_row);
+            victim = (int)std::min<size_t>((size_t)victim, fit);
+        }
+    }
+    pool_ = k + victim;
     d_slot_k_.alloc((size_t)B * no_ * pool_ * d * esz);
     d_slot_v_.alloc((size_t)B * no_ * pool_ * d * esz);
     d_win_k_.alloc((size_t)B * no_ * std::max<size_t>(wrows, 1) * d * esz);
@@ -212,6 +225,7 @@ void Engine::allocate() {
     d_entry_slot_.alloc(sizeof(int32_t) * B * no_ * k);
     d_slot_tok_.alloc(sizeof(int32_t) * B * no_ * pool_ + 64);
     d_slot_age_.alloc(sizeof(int32_t) * B * no_ * pool_);
+    d_vhead_.alloc(sizeof(int) * std::max(B * no_, 1));  // zeroed
     d_tok2slot_.alloc(sizeof(int32_t) * B * no_ * (size_t)nmax_);
     // empty pool: no token in any slot (-1), no slot for any token (-1), ages
     // kSlotEmpty (-1: oldest)
@@ -272,7 +286,7 @@ void Engine::allocate() {
     }
 
     // TMA tensor maps over the cache slots for the tensor-core attention:
-    // [B*NO*k rows][d] bf16, boxes of 64 columns x 16 or 32 rows, 128-byte
+    // [B*NO*pool rows][d] bf16 (entry areas: rows o*pool + [0, k)), boxes of 64 columns x 16 or 32 rows, 128-byte
     // swizzle (the kernel's stage layout). cuTensorMapEncodeTiled comes from
     // the driver through the runtime's entry-point query (no -lcuda).
     static const bool no_tma_slots = [] {  // CLO_ATTN_NOTMA=1: slot tiles by LDGSTS (experiment switch)
@@ -287,13 +301,13 @@ void Engine::allocate() {
         cudaDriverEntryPointQueryResult q{};
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
             auto encode = reinterpret_cast<EncodeFn>(fn);
-            CUtensorMap maps[2];
+            CUtensorMap maps[4];
             bool ok = true;
             const cuuint64_t rows = (cuuint64_t)B * no_ * pool_;
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < 4; ++i) {
                 const cuuint64_t dims[2] = {(cuuint64_t)d, rows};
                 const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-                const cuuint32_t box[2] = {64, 1};  // one row per box: loaded 4 at a time (tile::gather4)
+                const cuuint32_t box[2] = {64, i < 2 ? 16u : 32u};
                 const cuuint32_t estr[2] = {1, 1};
                 ok = ok && encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (i & 1) ? d_slot_v_.p : d_slot_k_.p,
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -339,6 +353,7 @@ void Engine::allocate() {
             bufs[13].alloc(sizeof(int32_t) * L * items * k, false);
             bufs[14].alloc(sizeof(int32_t) * L * items * k, false);
             bufs[15].alloc(sizeof(int) * L * items);
+            bufs[16].alloc(sizeof(int32_t) * L * items * k, false);
         }
         sc.count = bufs[0].as<int>();
         sc.items = bufs[1].as<SelItem>();
@@ -356,6 +371,7 @@ void Engine::allocate() {
         sc.fetch_tok = bufs[13].as<int32_t>();
         sc.fetch_slot = bufs[14].as<int32_t>();
         sc.fetch_count = bufs[15].as<int>();
+        sc.fetch_dem = bufs[16].as<int32_t>();
     }
 
     CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
@@ -450,6 +466,7 @@ EngineView Engine::view() const {
     v.slot_age = d_slot_age_.as<int32_t>();
     v.tok2slot = d_tok2slot_.as<int32_t>();
     v.pool = pool_;
+    v.vhead = d_vhead_.as<int>();
     v.codes = d_codes_.as<uint64_t>();
     v.code_stride = code_stride_;
     v.proj_t = d_proj_t_.as<double>();
@@ -486,6 +503,8 @@ EngineView Engine::view() const {
         const char* tm = d_tmaps_.as<char>();
         v.tmap_k = tm;
         v.tmap_v = tm + sizeof(CUtensorMap);
+        v.tmap_k32 = tm + 2 * sizeof(CUtensorMap);
+        v.tmap_v32 = tm + 3 * sizeof(CUtensorMap);
     }
     v.HQg = world_ * s.num_q_heads;
     v.q0 = rank_ * s.num_q_heads;
@@ -594,12 +613,17 @@ void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
     ra.sel = sc.sel;
     ra.fetch_tok = sc.fetch_tok;
     ra.fetch_slot = sc.fetch_slot;
+    ra.fetch_dem = sc.fetch_dem;
     ra.fetch_count = sc.fetch_count;
     ra.items_cap = (int)items;
     ra.layer = layer;
     ra.fresh = fresh;
     prof_begin(st);
     launch_reconcile(ra, st);
+    if (!fresh && pool_ > cfg_.k) {
+        launch_demote(gather_args(layer, 0), st);  // leaving rows -> victim areas, before the gather
+        launches_ += 1;
+    }
     prof_end(st, "reconcile", layer);
     launches_ += 1;
 }
@@ -612,6 +636,7 @@ GatherEngineArgs Engine::gather_args(int layer, int count_bytes) const {
     ga.count = sc.count;
     ga.fetch_tok = sc.fetch_tok;
     ga.fetch_slot = sc.fetch_slot;
+    ga.fetch_dem = sc.fetch_dem;
     ga.fetch_count = sc.fetch_count;
     ga.items_cap = cfg_.batch * cfg_.shape.num_kv_heads;
     ga.layer = layer;

@@ -98,7 +98,7 @@ class Engine {
 
     DevBuf d_persistent_, d_pidx_, d_oidx_, d_tau_, d_qimp_;
     DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;
-    DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_slot_age_, d_tok2slot_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
+    DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_slot_age_, d_tok2slot_, d_vhead_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
     DevBuf d_hits_, d_misses_, d_cache_last_, d_entry_last_, d_last_hit_, d_history_, d_gathered_;
     DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_, d_xfer_, d_off_layers_;
     int n_off_layers_ = 0;
@@ -113,7 +113,7 @@ class Engine {
     std::array<bool, 2> in_used_{};
     int pending_free_ = -1;  // slot whose consumer graph is being launched
     std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
-    std::array<std::array<DevBuf, 16>, 2> scratch_bufs_;
+    std::array<std::array<DevBuf, 17>, 2> scratch_bufs_;
 
     cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_xfer_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr;

@@ -63,8 +63,9 @@ struct SelScratch {
     int* need;             // [B*H] ties to take / remaining k during radix passes
     uint32_t* radix_hist;  // [B*H][256] exact radix pass histogram
     int32_t* sel;          // [B*H][k] offloaded items: the new selection (ascending)
-    int32_t* fetch_tok;    // [L][B*H][k] rows to fetch over PCIe (token, destination slot)
-    int32_t* fetch_slot;   // [L][B*H][k]
+    int32_t* fetch_tok;    // [L][B*H][k] move list: source (host token, or -(victim slot + 1))
+    int32_t* fetch_slot;   // [L][B*H][k]   destination entry slot
+    int32_t* fetch_dem;    // [L][B*H][k]   victim slot the leaving row moves to first, or -1
     int* fetch_count;      // [L][B*H]
 };
 
@@ -102,6 +103,7 @@ struct EngineView {
     int32_t* slot_age;     // [B*NO][pool] step the slot's token left the entry
     int32_t* tok2slot;     // [B*NO][nmax] slot of each resident token (-1: not in HBM)
     int pool;              // slots per offloaded head (k + victim rows)
+    int* vhead;            // [B*NO] FIFO cursor over each head's victim area (offset in [0, victim))
     uint64_t* codes;
     int64_t code_stride;   // u64 words per segment (even)
     const double* proj_t;
@@ -141,11 +143,13 @@ struct EngineView {
     unsigned* xflag[kMaxRanks];  // rank r's per-layer arrival counters [L]
     unsigned long long xtimeout_ns;  // a peer silent this long is reported lost
     // TMA tensor maps (CUtensorMap, 64-byte aligned, device memory) over the
-    // row pool [B*NO*pool][d] bf16: 128-byte swizzled boxes of 64 columns x 1
-    // row, loaded 4 arbitrary rows at a time (tile::gather4) in entry order;
-    // null when not built (f32 rows, other d)
-    const void* tmap_k;    // one-row boxes over the pool [B*NO*pool][d]: TMA gather4
+    // row pools [B*NO*pool][d] bf16 (row o*pool + slot): 128-byte swizzled
+    // boxes of 64 columns x the attention tile rows, read over the entry area
+    // (slots [0, k)); null when not built (f32 rows, other d)
+    const void* tmap_k;    // 16-row boxes
     const void* tmap_v;
+    const void* tmap_k32;  // 32-row boxes
+    const void* tmap_v32;
 };
 
 }  // namespace clo

@@ -50,64 +50,43 @@ __device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
     return lo;
 }
 
-// Reconcile of one missed head's entry with its new selection over the head's
-// HBM row pool (one CTA per head; kRecThreads threads):
-//   1. the old entry's slots become eviction candidates, aged `t` (now);
-//   2. every new token already resident in the pool (tok2slot) keeps its
-//      slot — whether it was in the old entry or left it at an earlier step;
-//   3. the remaining tokens take the least recently vacated slots (never
-//      filled first, then by the step they left the entry, ties by slot
-//      index): a two-pass 8-bit radix select over the 16-bit keys age + 1;
-//   4. evicted tokens leave tok2slot; the new ones enter it and go on the
-//      fetch list (token ascending, as the selection).
-// The entry's contents are exactly the reference's (update_entry,
-// similarity_cache.cpp:74-87); only which rows cross PCIe changes.
+// Reconcile of one missed head's entry with its new selection (one CTA per
+// head). A head's HBM rows are a pool: the ENTRY AREA, slots [0, k), holds
+// the entry's rows (CacheEntry::k_rows/v_rows, in slot order; entry_slot maps
+// entry position -> slot) and is what attention streams; the VICTIM AREA,
+// slots [k, pool), keeps rows that left the entry lately.
+//   1. new tokens already in the entry area keep their slot;
+//   2. the other new tokens take the entry slots the leaving tokens free
+//      (both in ascending order). Each arrives from the victim area if it is
+//      resident there (a promotion, an HBM copy), else over PCIe;
+//   3. each leaving token's row is demoted into the victim area, a FIFO ring
+//      per head: the slots after the head's cursor (demoted longest ago, or
+//      emptied by promotions) are overwritten first; this step's promotion
+//      sources are skipped.
+// Demotions are copied by demote_kernel (after this kernel, before the
+// gather); promotions and host fetches are the gather kernels' move list. The entry's contents are exactly
+// the reference's (update_entry, similarity_cache.cpp:74-87); only which rows
+// cross PCIe changes.
+//
+// Move list of item i (fetch_*[layer][i][j], j < fetch_count): fetch_slot =
+// destination entry slot; fetch_tok = source token (host row) when >= 0, or
+// -(victim slot + 1) for a promotion; fetch_dem = the victim slot the slot's
+// leaving row is demoted to (demote_kernel), or -1.
 __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a) {
     using Scan = cub::BlockScan<int, kRecThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int s_hist[256];
-    __shared__ int s_digit, s_below;
+    __shared__ int s_nprom;
     extern __shared__ int32_t rs[];
     const EngineView& v = a.v;
-    const int k = v.k, P = v.pool;
+    const int k = v.k, P = v.pool, V = P - k;
     int32_t* nsel = rs;            // [k] new selection (ascending)
-    int32_t* need_pos = rs + k;    // [k] entry positions whose token is not resident
-    int32_t* victims = rs + 2 * k; // [k] slots they take (ascending)
+    int32_t* need_pos = rs + k;    // [k] entry positions of the incoming tokens
+    int32_t* freed = rs + 2 * k;   // [k] freed entry slots (ascending); first a kept flag per slot
+    int32_t* dvict = rs + 3 * k;   // [k] demotion targets (ascending victim slots)
     const int count = a.count[a.layer];
     const int t = a.fresh ? 0 : *v.dev_step + 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (k + kRecThreads - 1) / kRecThreads;
     const int r0 = threadIdx.x * per, r1 = min(k, r0 + per);
-    const int pper = (P + kRecThreads - 1) / kRecThreads;
-    const int p0 = threadIdx.x * pper, p1 = min(P, p0 + pper);
-    // smallest-first digit search over s_hist: the digit holding the
-    // `want`-th smallest candidate and the count below it (warp 0)
-    auto pick_digit = [&](int want) {
-        if (warp == 0) {
-            int running = 0, D = -1, below = 0;
-            for (int b0 = 0; b0 < 256 && D < 0; b0 += 32) {
-                const int x = s_hist[b0 + lane];
-                int incl = x;
-#pragma unroll
-                for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o2);
-                    if (lane >= o2) incl += y;
-                }
-                const unsigned hit = __ballot_sync(0xffffffffu, running + incl >= want);
-                if (hit) {
-                    const int first = __ffs(hit) - 1;
-                    below = running + __shfl_sync(0xffffffffu, incl - x, first);
-                    D = b0 + first;
-                }
-                running += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) {
-                s_digit = D;
-                s_below = below;
-            }
-        }
-        __syncthreads();
-    };
     for (int item = blockIdx.x; item < count; item += gridDim.x) {
         const int seg = a.items[item].seg;
         const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
@@ -120,87 +99,99 @@ __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a)
         const int32_t* sel = a.sel + (size_t)item * k;
         for (int i = threadIdx.x; i < k; i += blockDim.x) {
             nsel[i] = sel[i];
-            if (!a.fresh) s_age[e_slot[i]] = t;  // 1) the old entry's rows become candidates
+            freed[i] = 0;  // kept flags of the entry slots
         }
+        if (threadIdx.x == 0) s_nprom = 0;
         __syncthreads();
-        // 2) resident tokens keep their slot
-        int nneed = 0;
+        // 1) classify the new tokens
+        int nin = 0, nprom = 0;
         for (int i = r0; i < r1; ++i) {
             const int s = t2s[nsel[i]];
-            if (s >= 0) {
-                s_age[s] = kSlotInEntry;
+            if (s >= 0 && s < k) {
+                freed[s] = 1;
                 e_slot[i] = s;
             } else {
-                ++nneed;
-            }
-        }
-        int nbase, total;
-        Scan(scan_tmp).ExclusiveSum(nneed, nbase, total);
-        for (int i = r0; i < r1; ++i)
-            if (t2s[nsel[i]] < 0) need_pos[nbase++] = i;
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
-        __syncthreads();
-        // 3) the `total` least recently vacated slots: key = age + 1 (empty -1 -> 0)
-        int T = 0, need_eq = 0;
-        if (total > 0) {
-            for (int p = p0; p < p1; ++p) {
-                const int ag = s_age[p];
-                if (ag != kSlotInEntry) atomicAdd(&s_hist[(ag + 1) >> 8], 1);
-            }
-            __syncthreads();
-            pick_digit(total);
-            const int D1 = s_digit, below1 = s_below;
-            for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
-            __syncthreads();
-            for (int p = p0; p < p1; ++p) {
-                const int ag = s_age[p];
-                if (ag != kSlotInEntry && ((ag + 1) >> 8) == D1) atomicAdd(&s_hist[(ag + 1) & 255], 1);
-            }
-            __syncthreads();
-            pick_digit(total - below1);
-            T = (D1 << 8) | s_digit;
-            need_eq = total - below1 - s_below;
-        }
-        int lt = 0, eq = 0;
-        if (total > 0)
-            for (int p = p0; p < p1; ++p) {
-                const int ag = s_age[p];
-                if (ag == kSlotInEntry) continue;
-                lt += ag + 1 < T;
-                eq += ag + 1 == T;
-            }
-        int lt_base, eq_base;
-        Scan(scan_tmp).ExclusiveSum(lt, lt_base);
-        __syncthreads();
-        Scan(scan_tmp).ExclusiveSum(eq, eq_base);
-        if (total > 0) {
-            int pos = lt_base + min(eq_base, need_eq), eq_seen = eq_base;
-            for (int p = p0; p < p1; ++p) {
-                const int ag = s_age[p];
-                if (ag == kSlotInEntry) continue;
-                const int key = ag + 1;
-                if (key < T) {
-                    victims[pos++] = p;
-                } else if (key == T) {
-                    if (eq_seen < need_eq) victims[pos++] = p;
-                    ++eq_seen;
+                ++nin;
+                if (s >= k) {
+                    s_age[s] = kSlotInEntry;  // promotion source: not a demotion target
+                    ++nprom;
                 }
             }
         }
+        if (nprom) atomicAdd(&s_nprom, nprom);
+        int nbase, total;
+        Scan(scan_tmp).ExclusiveSum(nin, nbase, total);
+        for (int i = r0; i < r1; ++i) {
+            const int s = t2s[nsel[i]];
+            if (s < 0 || s >= k) need_pos[nbase++] = i;
+        }
         __syncthreads();
-        // 4) evict, insert, publish the fetch list (token ascending)
+        // 2) freed entry slots, ascending (exactly `total` of them)
+        int nf = 0;
+        for (int e = r0; e < r1; ++e) nf += !freed[e];
+        int fbase;
+        Scan(scan_tmp).ExclusiveSum(nf, fbase);
+        static_assert(kRecThreads * 8 >= 8192, "per-thread freed-slot list covers k <= reconcile_max_k()");
+        int fl[8];  // this thread's freed slots (per <= 8)
+        int nfl = 0;
+        for (int e = r0; e < r1; ++e)
+            if (!freed[e]) fl[nfl++] = e;
+        __syncthreads();  // every kept flag read before the list overwrites them
+        for (int i = 0; i < nfl; ++i) freed[fbase + i] = fl[i];
+        // 3) demotion targets: the victim area is a FIFO ring walked by a
+        //    per-head cursor, so the slots after the cursor hold the rows
+        //    demoted longest ago (or emptied by promotions). Take the next
+        //    ndem slots in ring order, skipping this step's promotion
+        //    sources; the window is at most total + nprom slots: O(moves).
+        int ndem = 0;
+        if (!a.fresh && total > 0 && V > 0) {
+            const int vh = v.vhead[o];
+            const int W = min(V, total + s_nprom);
+            const int wper = (W + kRecThreads - 1) / kRecThreads;
+            const int q0 = threadIdx.x * wper, q1 = min(W, q0 + wper);
+            int nc = 0;
+            for (int q = q0; q < q1; ++q) nc += s_age[k + (vh + q) % V] != kSlotInEntry;
+            int cbase, ncand;
+            Scan(scan_tmp).ExclusiveSum(nc, cbase, ncand);
+            ndem = min(total, ncand);
+            for (int q = q0; q < q1 && cbase < ndem; ++q) {
+                const int p = k + (vh + q) % V;
+                if (s_age[p] == kSlotInEntry) continue;
+                dvict[cbase] = p;
+                if (++cbase == ndem) v.vhead[o] = (vh + q + 1) % V;  // past the last slot taken
+            }
+        }
+        __syncthreads();
+        // 4) pair incoming j -> freed slot j (-> its leaving row demoted to dvict[j]);
+        //    update the maps to the state after the gather's moves
         int32_t* ftok = a.fetch_tok + ((size_t)a.layer * a.items_cap + item) * k;
         int32_t* fslot = a.fetch_slot + ((size_t)a.layer * a.items_cap + item) * k;
+        int32_t* fdem = a.fetch_dem + ((size_t)a.layer * a.items_cap + item) * k;
         for (int j = threadIdx.x; j < total; j += blockDim.x) {
-            const int vs = victims[j], pos = need_pos[j], tok = nsel[pos];
-            const int old = s_tok[vs];
-            if (old >= 0) t2s[old] = -1;  // old is not in the new selection (its slot was a candidate)
-            t2s[tok] = vs;
-            s_tok[vs] = tok;
-            s_age[vs] = kSlotInEntry;
-            e_slot[pos] = vs;
-            ftok[j] = tok;
-            fslot[j] = vs;
+            const int e = freed[j], pos = need_pos[j], tok = nsel[pos];
+            const int x = s_tok[e];  // the leaving token (-1 before the first fill)
+            const int s = t2s[tok];  // >= k: resident in the victim area
+            int dem = -1;
+            if (j < ndem && x >= 0) {
+                dem = dvict[j];
+                const int y = s_tok[dem];
+                if (y >= 0) t2s[y] = -1;  // evicted (y is in neither selection)
+                t2s[x] = dem;
+                s_tok[dem] = x;
+                s_age[dem] = t;
+            } else if (x >= 0) {
+                t2s[x] = -1;
+            }
+            if (s >= k) {  // promotion: the victim slot empties
+                s_tok[s] = -1;
+                s_age[s] = kSlotEmpty;
+            }
+            t2s[tok] = e;
+            s_tok[e] = tok;
+            e_slot[pos] = e;
+            ftok[j] = s >= k ? -(s + 1) : tok;
+            fslot[j] = e;
+            fdem[j] = dem;
         }
         for (int i = threadIdx.x; i < k; i += blockDim.x) e_idx[i] = nsel[i];
         if (threadIdx.x == 0) a.fetch_count[(size_t)a.layer * a.items_cap + item] = total;
@@ -208,11 +199,14 @@ __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a)
     }
 }
 
-// Work units = (missed head, matrix, block of fetch-list vectors). K and V are
+// Work units = (missed head, matrix, block of move-list vectors). K and V are
 // separate units (all of a head's K rows, then its V rows) so a CTA's
 // outstanding reads stay within one host matrix region at a time.
 // Interleaved host K|V (v.kv_fused): one unit covers whole 2*d-element token
 // runs, split into the K and V slots on the way out.
+// Per vector: load the source (host row over PCIe, or the victim slot of a
+// promotion) and store it into the entry slot (its leaving row was demoted by
+// reconcile).
 __device__ __forceinline__ int gather_units_per_item(const EngineView& v) {
     const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
     if (v.kv_fused) return (v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs;
@@ -225,127 +219,102 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
     const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);  // host row pitch
-    if (v.kv_fused) {  // token runs [K row | V row] of 2*vpr vectors
-        const int vpt = 2 * vpr;
-        const int upi = (v.k * vpt + kUnitVecs - 1) / kUnitVecs;
-        const int item = u / upi, part = u % upi;
-        const size_t li = (size_t)layer * a.items_cap + item;
-        const int v0 = part * kUnitVecs;
-        const int v1 = min(a.fetch_count[li] * vpt, v0 + kUnitVecs);
-        if (v0 >= v1) return;
-        const int seg = a.items[li].seg;
-        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
-        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
-        const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-        const uint4* src = reinterpret_cast<const uint4*>((const char*)v.host_k + base * dtype_size(v.kv_dtype));
-        uint4* dk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.pool * row_bytes);
-        uint4* dv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * row_bytes);
-        const int32_t* ftok = a.fetch_tok + li * v.k;
-        const int32_t* fslot = a.fetch_slot + li * v.k;
-        uint4 r[kUnitUnroll];
-        uint4* dp[kUnitUnroll];
-#pragma unroll
-        for (int uu = 0; uu < kUnitUnroll; ++uu) {
-            const int e = v0 + uu * kGatherThreads + threadIdx.x;
-            if (e < v1) {
-                const int row = e / vpt, c = e - row * vpt;
-                dp[uu] = c < vpr ? dk + (size_t)fslot[row] * vpr + c : dv + (size_t)fslot[row] * vpr + (c - vpr);
-                r[uu] = src[(size_t)ftok[row] * rvpr + c];
-            }
-        }
-#pragma unroll
-        for (int uu = 0; uu < kUnitUnroll; ++uu) {
-            const int e = v0 + uu * kGatherThreads + threadIdx.x;
-            if (e < v1) *dp[uu] = r[uu];
-        }
-        if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
-        return;
-    }
-    const int parts = (v.k * vpr + kUnitVecs - 1) / kUnitVecs;  // per matrix
-    const int units_per_item = 2 * parts;
-    const size_t esz = dtype_size(v.kv_dtype);
-    const int item = u / units_per_item, rem = u % units_per_item;
-    const int mat = rem / parts, part = rem % parts;  // mat 0 = K, 1 = V
+    const bool fused = v.kv_fused;
+    const int vpt = fused ? 2 * vpr : vpr;  // vectors per moved row (per matrix when split)
+    const int upm = (v.k * vpt + kUnitVecs - 1) / kUnitVecs;
+    const int upi = fused ? upm : 2 * upm;
+    const int item = u / upi, rem = u % upi;
+    const int mat = fused ? 0 : rem / upm, part = fused ? rem : rem % upm;  // mat 0 = K, 1 = V
     const size_t li = (size_t)layer * a.items_cap + item;
-    const int nf = a.fetch_count[li];
     const int v0 = part * kUnitVecs;
-    const int v1 = min(nf * vpr, v0 + kUnitVecs);
+    const int v1 = min(a.fetch_count[li] * vpt, v0 + kUnitVecs);
     if (v0 >= v1) return;
-    const int seg = a.items[(size_t)layer * a.items_cap + item].seg;
+    const int seg = a.items[li].seg;
     const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
     const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
     const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-    const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
-    uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
+    const size_t esz = dtype_size(v.kv_dtype);
+    const uint4* hsrc = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
+    uint4* pk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.pool * row_bytes);
+    uint4* pv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * row_bytes);
     const int32_t* ftok = a.fetch_tok + li * v.k;
     const int32_t* fslot = a.fetch_slot + li * v.k;
     uint4 r[kUnitUnroll];
-    size_t dsto[kUnitUnroll];
+    uint4* dp[kUnitUnroll];
+    int host = 0;
 #pragma unroll
     for (int uu = 0; uu < kUnitUnroll; ++uu) {
         const int e = v0 + uu * kGatherThreads + threadIdx.x;
         if (e < v1) {
-            const int row = e / vpr, c = e - row * vpr;
-            dsto[uu] = (size_t)fslot[row] * vpr + c;
-            r[uu] = src[(size_t)ftok[row] * rvpr + c];
+            const int row = e / vpt, c = e - row * vpt;
+            // vector c of the moved row: K part (c < vpr) or V part (fused), or matrix `mat`
+            const bool isv = fused ? c >= vpr : mat == 1;
+            const int cc = fused && isv ? c - vpr : c;
+            uint4* pool = isv ? pv : pk;
+            const int slot = fslot[row], src = ftok[row];
+            dp[uu] = pool + (size_t)slot * vpr + cc;
+            if (src >= 0) {
+                r[uu] = hsrc[(size_t)src * rvpr + c];  // PCIe: host row (K|V run when fused)
+                ++host;
+            } else {
+                r[uu] = pool[(size_t)(-src - 1) * vpr + cc];  // promotion from the victim area
+            }
         }
     }
 #pragma unroll
     for (int uu = 0; uu < kUnitUnroll; ++uu) {
         const int e = v0 + uu * kGatherThreads + threadIdx.x;
-        if (e < v1) dst[dsto[uu]] = r[uu];
+        if (e < v1) *dp[uu] = r[uu];
     }
-    if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+    if (a.count_bytes) {
+        host = __reduce_add_sync(0xffffffffu, host);
+        if ((threadIdx.x & 31) == 0 && host) atomicAdd(v.gathered_bytes, (unsigned long long)host * 16ull);
+    }
 }
 
-// Light variant of the engine gather (CLO_GATHER=lite): the same LSU copy
-// with T threads x U 16-byte loads in flight per CTA and 32-bit slot offsets,
-// sized (registers, no shared memory) to co-reside on an SM with one
-// attention CTA, so the transfer stream's CTAs do not take whole SMs away from
-// the compute stream. Unit = (missed head, matrix, T*U vectors).
-template <int T, int U>
-__global__ void __launch_bounds__(T) gather_lite_kernel(const __grid_constant__ GatherEngineArgs a) {
+// Demotions of one layer (after reconcile, before the gather, on the
+// selection stream): every leaving row the reconcile paired with a victim
+// slot is copied entry slot -> victim slot, 16-byte vectors over the whole
+// grid (HBM -> HBM). Unit = (item, 2 * vpr * kUnitUnroll... vectors).
+__global__ void __launch_bounds__(kGatherThreads) demote_kernel(GatherEngineArgs a) {
     const EngineView& v = a.v;
-    const int row_bytes = v.d * dtype_size(v.kv_dtype);
-    const int vpr = row_bytes / 16;
-    const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);  // host row pitch
-    constexpr int kVecs = T * U;
-    const int parts = (v.k * vpr + kVecs - 1) / kVecs;
-    const int upi = 2 * parts;
+    const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
+    const int per_item = v.k * 2 * vpr;  // vectors if every move demotes
+    const int upi = (per_item + kUnitVecs - 1) / kUnitVecs;
     const int units = a.count[a.layer] * upi;
-    const size_t esz = dtype_size(v.kv_dtype);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int item = u / upi, rem = u - item * upi;
-        const int mat = rem / parts, part = rem - mat * parts;
+        const int item = u / upi, part = u % upi;
         const size_t li = (size_t)a.layer * a.items_cap + item;
-        const int v0 = part * kVecs;
-        const int v1 = min(a.fetch_count[li] * vpr, v0 + kVecs);
-        if (v0 >= v1) continue;
+        const int n = a.fetch_count[li] * 2 * vpr;
+        const int v0 = part * kUnitVecs;
+        if (v0 >= n) continue;
         const int seg = a.items[li].seg;
         const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
         const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
-        const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-        const uint4* src = reinterpret_cast<const uint4*>((const char*)(mat ? v.host_v : v.host_k) + base * esz);
-        uint4* dst = reinterpret_cast<uint4*>((char*)(mat ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
-        const int32_t* ftok = a.fetch_tok + li * v.k;
+        uint4* pk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.pool * (size_t)vpr * 16);
+        uint4* pv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * (size_t)vpr * 16);
         const int32_t* fslot = a.fetch_slot + li * v.k;
-        uint4 r[U];
-        int dsto[U];
+        const int32_t* fdem = a.fetch_dem + li * v.k;
+        uint4 buf[kUnitUnroll];
+        uint4* to[kUnitUnroll];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-            const int e = v0 + uu * T + (int)threadIdx.x;
-            if (e < v1) {
-                const int row = e / vpr, c = e - row * vpr;
-                dsto[uu] = fslot[row] * vpr + c;
-                r[uu] = src[(size_t)ftok[row] * rvpr + c];
+        for (int uu = 0; uu < kUnitUnroll; ++uu) {
+            const int x = v0 + uu * kGatherThreads + threadIdx.x;
+            to[uu] = nullptr;
+            if (x < n) {
+                const int j = x / (2 * vpr), c = x - j * 2 * vpr;
+                const int dem = fdem[j];
+                if (dem >= 0) {
+                    uint4* pool = c < vpr ? pk : pv;
+                    const int cc = c < vpr ? c : c - vpr;
+                    buf[uu] = pool[(size_t)fslot[j] * vpr + cc];
+                    to[uu] = pool + (size_t)dem * vpr + cc;
+                }
             }
         }
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-            const int e = v0 + uu * T + (int)threadIdx.x;
-            if (e < v1) dst[dsto[uu]] = r[uu];
-        }
-        if (a.count_bytes && threadIdx.x == 0) atomicAdd(v.gathered_bytes, (unsigned long long)(v1 - v0) * 16ull);
+        for (int uu = 0; uu < kUnitUnroll; ++uu)
+            if (to[uu]) *to[uu] = buf[uu];
     }
 }
 
@@ -539,6 +508,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     __shared__ __align__(8) uint64_t tbar[kTmaWarps][kTmaMaxStages];
     const EngineView& v = a.v;
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int vpr = row_bytes / 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gpm = (v.k + kTmaRows - 1) / kTmaRows;  // 32-row groups per matrix
     const bool fused = v.kv_fused;                    // one [K|V] token run per lane and group
@@ -555,82 +525,108 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    // group i of this warp -> (rows, host source of lane's row, slot destination)
-    auto locate = [&](int i, int& rows, const char*& src, char*& dst, char*& dst2) {
+    // Row of group i handled by this lane: destination entry slot in its
+    // matrix (K, or K then V for fused runs), source = the host row (`host`
+    // set) or the victim slot `prom` of a promotion (the slot's leaving row was
+    // demoted by reconcile already).
+    struct Row {
+        int rows, mat, slot, prom;
+        size_t o;
+        const char* host;
+    };
+    auto locate = [&](int i) {
+        Row r{};
         const int gidx = gw + i * nw;
-        const int item = gidx / (nmat * gpm), rem = gidx % (nmat * gpm), mat = rem / gpm, grp = rem % gpm;
+        const int item = gidx / (nmat * gpm), rem = gidx % (nmat * gpm), grp = rem % gpm;
+        r.mat = rem / gpm;
         const size_t li = (size_t)a.layer * a.items_cap + item;
         const int nf = a.fetch_count[li];
-        rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
-        src = nullptr;
-        dst = nullptr;
-        dst2 = nullptr;
-        if (lane < rows) {
+        r.rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
+        r.prom = -1;
+        if (lane < r.rows) {
             const int seg = a.items[li].seg;
             const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
-            const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
-            const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
-            const int r = grp * kTmaRows + lane;
-            src = (const char*)(mat ? v.host_v : v.host_k) + (base + (size_t)a.fetch_tok[li * v.k + r] * v.row_stride) * dtype_size(v.kv_dtype);
-            dst = (char*)(mat ? v.slot_v : v.slot_k) + (o * v.pool + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
-            if (fused) dst2 = (char*)v.slot_v + (o * v.pool + a.fetch_slot[li * v.k + r]) * (size_t)row_bytes;
+            r.o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+            const int j = grp * kTmaRows + lane;
+            r.slot = a.fetch_slot[li * v.k + j];
+            const int src = a.fetch_tok[li * v.k + j];
+            if (src >= 0) {
+                const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+                r.host = (const char*)(r.mat ? v.host_v : v.host_k) + (base + (size_t)src * v.row_stride) * dtype_size(v.kv_dtype);
+            } else {
+                r.prom = -src - 1;
+            }
         }
+        return r;
+    };
+    auto row_ptr = [&](int m, size_t o, int slot) {  // pool row `slot` of matrix m
+        return (char*)(m ? v.slot_v : v.slot_k) + (o * v.pool + slot) * (size_t)row_bytes;
     };
     auto load = [&](int i) {
-        int rows;
-        const char* src;
-        char *dst, *dst2;
-        locate(i, rows, src, dst, dst2);
+        const Row r = locate(i);
         const int s = i % stages;
         uint64_t* bar = &tbar[warp][s];
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (rows)
+            if (r.rows)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                             "r"(rows * cbytes)
+                             "r"(r.rows * cbytes)
                              : "memory");
             else
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
         }
         __syncwarp();
-        if (lane < rows)
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes)),
-                "l"(src), "r"(cbytes), "r"(smem_u32(bar))
-                : "memory");
+        if (lane < r.rows) {
+            const uint32_t dst = smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes);
+            if (r.prom < 0) {  // over PCIe from pinned host memory
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "l"(r.host), "r"(cbytes), "r"(smem_u32(bar))
+                    : "memory");
+            } else {  // promotion: the victim slot's row(s) in HBM
+                for (int m = 0; m < (fused ? 2 : 1); ++m) {  // fused: K then V row of the slot
+                    const int mm = fused ? m : r.mat;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst + m * row_bytes),
+                        "l"(row_ptr(mm, r.o, r.prom)), "r"(row_bytes), "r"(smem_u32(bar))
+                        : "memory");
+                }
+            }
+        }
     };
     for (int i = 0; i < min(stages, mine); ++i) load(i);
     unsigned long long moved = 0;
     for (int i = 0; i < mine; ++i) {
         const int s = i % stages;
-        int rows;
-        const char* src;
-        char *dst, *dst2;
-        locate(i, rows, src, dst, dst2);
+        const Row r = locate(i);
         asm volatile(
             "{\n\t.reg .pred p;\n\tW_%=:\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
             "@!p bra W_%=;\n\t}" ::"r"(smem_u32(&tbar[warp][s])),
             "r"((i / stages) & 1)
             : "memory");
-        if (lane < rows) {
+        if (lane < r.rows) {
             const uint32_t sa = smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa),
-                         "r"(row_bytes)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                             row_ptr(fused ? 0 : r.mat, r.o, r.slot)),
+                         "r"(sa), "r"(row_bytes)
                          : "memory");
             if (fused)
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst2),
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                 row_ptr(1, r.o, r.slot)),
                              "r"(sa + row_bytes), "r"(row_bytes)
                              : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage reusable
+            if (r.prom < 0) moved += (unsigned long long)cbytes;
         }
-        moved += (unsigned long long)rows * cbytes;
         __syncwarp();
         if (i + stages < mine) load(i + stages);
     }
-    if (lane < 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) moved += __shfl_xor_sync(0xffffffffu, moved, o2);
     if (a.count_bytes && lane == 0 && moved) atomicAdd(v.gathered_bytes, moved);
 }
 
@@ -647,7 +643,7 @@ void launch_gather_tma_op(const void* src, void* dst, const int32_t* idx, int ro
 }
 
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
-    const size_t sm = sizeof(int32_t) * 3 * (size_t)a.v.k;
+    const size_t sm = sizeof(int32_t) * 4 * (size_t)a.v.k;  // nsel, need_pos, freed, dvict
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(reconcile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int grid = a.items_cap < 1024 ? a.items_cap : 1024;
@@ -662,20 +658,13 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 // regions, where each row's host-address translation misses, the LSU copy
 // (48 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
 // outstanding and wins (512K: +8%, 1M: +20%).
-// CLO_GATHER=lsu|tma|lite[:T,U] forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
+// CLO_GATHER=lsu|tma forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
 void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stream) {
-    static const int mode = [] {  // 0 auto, 1 lsu, 2 tma, else lite T*100+U
+    static const int mode = [] {  // 0 auto, 1 lsu, 2 tma
         const char* e = getenv("CLO_GATHER");
         if (!e || !*e) return 0;
         const std::string m(e);
-        if (m == "lsu") return 1;
-        if (m == "tma") return 2;
-        if (m.rfind("lite", 0) == 0) {
-            int t = 128, u = 8;
-            sscanf(e, "lite:%d,%d", &t, &u);
-            return t * 100 + u;
-        }
-        return 0;
+        return m == "lsu" ? 1 : (m == "tma" ? 2 : 0);
     }();
     static const int2 shape = [] {
         int2 r{1, 1};
@@ -701,31 +690,20 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
         gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
         return;
     }
-    if (use > 2) {
-        const int t = use / 100, u = use % 100;
-        const int64_t units = (int64_t)a.items_cap * 2 * ((v.k * vpr + t * u - 1) / (t * u));
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : kNumSMs, units));
-        switch (use) {
-            case 12804:
-                gather_lite_kernel<128, 4><<<grid, 128, 0, stream>>>(a);
-                return;
-            case 25604:
-                gather_lite_kernel<256, 4><<<grid, 256, 0, stream>>>(a);
-                return;
-            case 6408:
-                gather_lite_kernel<64, 8><<<grid, 64, 0, stream>>>(a);
-                return;
-            default:
-                gather_lite_kernel<128, 8><<<grid, 128, 0, stream>>>(a);
-                return;
-        }
-    }
     // PCIe needs well over 100 KB in flight; 48 CTAs x 32 KiB saturate the
     // link and leave most SMs to the selection and attention kernels.
     const int64_t units = v.kv_fused ? (int64_t)a.items_cap * ((v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs)
                                      : (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
+}
+
+void launch_demote(const GatherEngineArgs& a, cudaStream_t stream) {
+    if (a.v.pool <= a.v.k) return;  // no victim area: nothing is ever demoted
+    const int vpr = a.v.d * dtype_size(a.v.kv_dtype) / 16;
+    const int64_t units = (int64_t)a.items_cap * ((a.v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, 4 * kNumSMs));
+    demote_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 
 void launch_publish(const GatherEngineArgs& a, cudaStream_t stream) { publish_kernel<<<1, 1, 0, stream>>>(a); }

@@ -12,8 +12,9 @@ struct ReconcileArgs {
     const SelItem* items;  // this layer's work list (missed offloaded heads)
     const int* count;      // [L]
     const int32_t* sel;    // [item][k] new ascending selections
-    int32_t* fetch_tok;    // [L][items_cap][k]
-    int32_t* fetch_slot;
+    int32_t* fetch_tok;    // [L][items_cap][k] source: host token (>= 0) or -(victim slot + 1)
+    int32_t* fetch_slot;   // destination entry slot
+    int32_t* fetch_dem;    // victim slot the slot's leaving row moves to first, or -1
     int* fetch_count;      // [L][items_cap]
     int items_cap;         // B*H
     int layer;
@@ -26,6 +27,7 @@ struct GatherEngineArgs {
     const int* count;      // [L]
     const int32_t* fetch_tok;
     const int32_t* fetch_slot;
+    const int32_t* fetch_dem;
     const int* fetch_count;
     int items_cap;
     int layer;
@@ -33,6 +35,9 @@ struct GatherEngineArgs {
 };  // items: base of the per-layer work lists [L][items_cap] (gather_unit offsets by layer)
 
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream);
+// Demotions of the layer's leaving rows into the victim areas (after
+// reconcile, before the gather); a no-op launch-free call without victim rows.
+void launch_demote(const GatherEngineArgs& a, cudaStream_t stream);
 // Row size must be a multiple of 16 bytes (d*sizeof(dtype) % 16 == 0).
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream);
 // GPU-centric transfer pipeline (one decode step): publish(l) after

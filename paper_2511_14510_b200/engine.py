@@ -71,7 +71,7 @@ class EngineConfig:  # engine.hpp:30-49 (+ B200 fields)
     kv_dtype: str = "bf16"
     kv_head_offset: int = 0
     device: int = 0
-    victim_rows: int = -1  # HBM rows kept per offloaded head beyond the entry (-1: auto = 2k, 0: none)
+    victim_rows: int = -1  # HBM rows kept per offloaded head beyond the entry (-1: auto = 8k capped by free HBM, 0: none)
 
     def to_c(self, n_prompt: int, max_steps: int) -> _lib.EngineConfigC:
         c = _lib.EngineConfigC()

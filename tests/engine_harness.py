@@ -86,46 +86,68 @@ def rel_l2(got, want):
 
 
 class PoolModel:
-    """The engine's HBM row pool of one offloaded head (gather.cu reconcile):
-    pool = k + victim rows; tokens already resident keep their slot, the rest
-    take the least recently vacated slots (empty first, then by the step
-    their token left the entry, ties by slot index). Returns how many rows
-    each reconcile fetches over PCIe."""
-    IN_ENTRY = 1 << 31
+    """The engine's HBM rows of one offloaded head (gather.cu reconcile): an
+    entry area of k slots (the entry, in slot order) and a victim area of
+    `victim` slots (2k when negative) holding rows that left the entry.
+    New tokens in the entry area keep their slot; the others take the slots
+    the leaving tokens free (ascending pairs), arriving from the victim area
+    when resident there (promotion) else over PCIe; each leaving row is
+    demoted into the victim area, a FIFO ring walked by a cursor (promotion
+    sources skipped).
+    reconcile() returns the rows fetched over PCIe."""
 
     def __init__(self, k, victim):
-        self.P = k + (2 * k if victim < 0 else victim)
+        self.k = k
+        self.P = k + (8 * k if victim < 0 else victim)
         self.slot_tok = [-1] * self.P
         self.age = [-1] * self.P
         self.t2s = {}
-        self.e_slot = []
+        self.vh = 0  # FIFO cursor over the victim area
 
     def reconcile(self, new_sel, t, fresh=False):
-        if not fresh:
-            for sl in self.e_slot:
-                self.age[sl] = t
-        e_new = [None] * len(new_sel)
-        need = []
+        k = self.k
+        new_sel = [int(x) for x in new_sel]
+        kept, need = set(), []
         for i, tok in enumerate(new_sel):
-            sl = self.t2s.get(int(tok))
-            if sl is None:
-                need.append(i)
+            sl = self.t2s.get(tok)
+            if sl is not None and sl < k:
+                kept.add(sl)
             else:
-                self.age[sl] = self.IN_ENTRY
-                e_new[i] = sl
-        cands = sorted((self.age[p] + 1, p) for p in range(self.P) if self.age[p] != self.IN_ENTRY)
-        victims = sorted(p for _, p in cands[:len(need)])
-        for vs, pos in zip(victims, need):
-            tok = int(new_sel[pos])
-            old = self.slot_tok[vs]
-            if old >= 0:
-                del self.t2s[old]
-            self.t2s[tok] = vs
-            self.slot_tok[vs] = tok
-            self.age[vs] = self.IN_ENTRY
-            e_new[pos] = vs
-        self.e_slot = e_new
-        return len(need)
+                need.append(i)
+        freed = [e for e in range(k) if e not in kept]
+        prom = {self.t2s[new_sel[i]] for i in need if new_sel[i] in self.t2s}
+        V = self.P - k
+        ndem, dv = 0, []
+        if not fresh and need and V > 0:  # FIFO ring from the cursor, skipping promotion sources
+            W = min(V, len(need) + len(prom))
+            cands = [(q, k + (self.vh + q) % V) for q in range(W) if k + (self.vh + q) % V not in prom]
+            ndem = min(len(need), len(cands))
+            dv = [p for _, p in cands[:ndem]]
+            if ndem:
+                self.vh = (self.vh + cands[ndem - 1][0] + 1) % V
+        host = 0
+        for j, pos in enumerate(need):
+            e, tok = freed[j], new_sel[pos]
+            x = self.slot_tok[e]
+            sl = self.t2s.get(tok)
+            if j < ndem and x >= 0:
+                w = dv[j]
+                y = self.slot_tok[w]
+                if y >= 0:
+                    del self.t2s[y]
+                self.t2s[x] = w
+                self.slot_tok[w] = x
+                self.age[w] = t
+            elif x >= 0:
+                del self.t2s[x]
+            if sl is not None:  # promotion: the victim slot empties
+                self.slot_tok[sl] = -1
+                self.age[sl] = -1
+            else:
+                host += 1
+            self.t2s[tok] = e
+            self.slot_tok[e] = tok
+        return host
 
 
 def run_and_compare(case, oracle, check_rows=True, tol=None):
