@@ -88,7 +88,7 @@ def rel_l2(got, want):
 class PoolModel:
     """The engine's HBM rows of one offloaded head (gather.cu reconcile): an
     entry area of k slots (the entry, in slot order) and a victim area of
-    `victim` slots (2k when negative) holding rows that left the entry.
+    `victim` slots (8k when negative) holding rows that left the entry.
     New tokens in the entry area keep their slot; the others take the slots
     the leaving tokens free (ascending pairs), arriving from the victim area
     when resident there (promotion) else over PCIe; each leaving row is
