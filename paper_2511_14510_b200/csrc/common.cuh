@@ -73,6 +73,20 @@ enum ErrBits : int {
     kErrAlias = 256,     // layer-aliased host store: a step's new K/V rows differ across layers
 };
 
+// Phase timestamps for latency diagnosis (build with EXTRA=-DCLO_PROBE; never
+// in the shipped library).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#ifdef CLO_PROBE
+#define CLO_PROBE_T(arr, i) \
+    if (threadIdx.x == 0) (arr)[i] = globaltimer_ns();
+#else
+#define CLO_PROBE_T(arr, i)
+#endif
+
 __device__ __forceinline__ void raise_err(int* flag, int bits) {
     if (flag) atomicOr(flag, bits);
 }

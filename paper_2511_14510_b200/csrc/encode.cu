@@ -1,5 +1,6 @@
 // encode.cu — K6 (prefill sign-hash encode), K5 (per-step append), helpers.
 #include "encode.cuh"
+#include "hash.cuh"
 #include "select.cuh"
 
 namespace clo {
@@ -63,9 +64,55 @@ __device__ __forceinline__ void store_row(void* base, size_t row, int d, const T
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
 }
 
-// One CTA per (sequence, KV head) of one layer.
+constexpr int kAppendTile = 16;  // new key rows hashed per pass of an append hash CTA
+
+template <typename T>
+__device__ __forceinline__ void append_hash(const EngineView& v, int l, int r) {
+    const int g = r / v.words, w = r % v.words;
+    const int lg = l * v.H + g;
+    const int t = *v.dev_step + 1;
+    const int row = v.n_prompt + t - 1;
+    extern __shared__ __align__(128) double hsm[];  // P slice [d][64], rows [kAppendTile][d]
+    double* ps = hsm;
+    double* xs = hsm + (size_t)v.d * 64;
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        bulk::mbar_init(&bar);
+        bulk::load_async(ps, v.proj_w + ((size_t)lg * v.words + w) * v.d * 64, (uint32_t)v.d * 64 * 8, &bar);
+    }
+    const T* nk = static_cast<const T*>(v.desc->new_k);
+    for (int b0 = 0; b0 < v.B; b0 += kAppendTile) {
+        const int nb = min(kAppendTile, v.B - b0);
+        if (b0 > 0) __syncthreads();  // the previous tile's chains are done with xs
+        for (int i = threadIdx.x; i < nb * v.d; i += blockDim.x) {
+            const int bb = b0 + i / v.d, c = i % v.d;
+            xs[i] = to_f64<T>(nk[(((size_t)bb * v.L + l) * v.H + g) * v.d + c]);
+        }
+        __syncthreads();
+        if (b0 == 0) bulk::wait(&bar, 0);
+        hash_word(ps, xs, v.d, nb, v.d, w, v.bits, [&](int j) {
+            const size_t seg = ((size_t)(b0 + j) * v.L + l) * v.H + g;
+            return reinterpret_cast<uint32_t*>(v.codes + seg * v.code_stride + (size_t)row * v.words);
+        });
+    }
+}
+
+// Phase 2 of one layer (engine.cpp:360-370). Two CTA roles in one grid:
+//   blockIdx.x <  B*H   one (sequence, KV head): the new K/V row into the
+//                       host store (or the persistent HBM store), the window
+//                       ring and the K mirror
+//   blockIdx.x >= B*H   one (KV head g, code word w): update_metadata's sign
+//                       bits (append_sign_row, retrieval.cpp:14-25) of the new
+//                       key of every sequence, word w only, against P's word
+//                       slice staged in shared memory by one bulk copy
+//                       (hash.cuh) -- P is read once per (g, w) instead of
+//                       once per sequence in dependent batches.
 template <typename T>
 __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l) {
+    if ((int)blockIdx.x >= v.B * v.H) {
+        append_hash<T>(v, l, (int)blockIdx.x - v.B * v.H);
+        return;
+    }
     const int b = blockIdx.x / v.H, g = blockIdx.x % v.H;
     const int lg = l * v.H + g;
     const int seg = (b * v.L + l) * v.H + g;
@@ -73,17 +120,14 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
     const int t = *v.dev_step + 1;
     const int row = v.n_prompt + t - 1;  // n_pool: the new token's index
     __shared__ T kr[kMaxHeadDim], vr[kMaxHeadDim];
-    __shared__ double kd[kMaxHeadDim];
     const size_t off = (((size_t)b * v.L + l) * v.H + g) * v.d;
     const T* nk = static_cast<const T*>(v.desc->new_k) + off;
     const T* nv = static_cast<const T*>(v.desc->new_v) + off;
     for (int i = threadIdx.x; i < v.d; i += blockDim.x) {
         kr[i] = nk[i];
         vr[i] = nv[i];
-        const double x = to_f64<T>(kr[i]);
-        if (!isfinite(x)) raise_err(v.err, kErrNonFiniteKey);
+        if (!isfinite(to_f64<T>(kr[i]))) raise_err(v.err, kErrNonFiniteKey);
         if (!isfinite(to_f64<T>(vr[i]))) raise_err(v.err, kErrNonFiniteValue);
-        kd[i] = x;
     }
     __syncthreads();
     if (pers) {
@@ -127,29 +171,6 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
             store_row<T>(v.win_v, o * wrows + v.sink + row % v.recent, v.d, vr);
         }
         if (v.kmirror) store_row<T>(v.kmirror, o * v.nmax + row, v.d, kr);
-    }
-    if (v.retriever == 1) {
-        uint32_t* out32 = reinterpret_cast<uint32_t*>(v.codes + (size_t)seg * v.code_stride + (size_t)row * v.words);
-        const double* pt = v.proj_t + (size_t)lg * v.d * v.bits;
-        for (int b0 = 0; b0 < v.words * 64; b0 += blockDim.x) {
-            const int bit = b0 + threadIdx.x;
-            double s = 0.0;
-            if (bit < v.bits && v.d == 128) {
-                double s1[1] = {0.0};
-                signhash_chain<128, 1>(pt + bit, (size_t)v.bits, kd, 128, s1);
-                s = s1[0];
-            } else if (bit < v.bits)
-                for (int c0 = 0; c0 < v.d; c0 += 32) {  // 32 loads in flight, sequential chain
-                    double p[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) p[i] = c0 + i < v.d ? pt[(size_t)(c0 + i) * v.bits + bit] : 0.0;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (c0 + i < v.d) s = dmac(s, p[i], kd[c0 + i]);
-                }
-            const unsigned bal = __ballot_sync(0xffffffffu, bit < v.bits && s >= 0.0);
-            if ((threadIdx.x & 31) == 0 && bit < v.words * 64) out32[bit >> 5] = bal;
-        }
     }
 }
 
@@ -228,10 +249,16 @@ void launch_encode(const EncodeSeg* segs_dev, int n_segs, int64_t n, int d, int 
 }
 
 void launch_append(const EngineView& v, int layer, cudaStream_t stream) {
-    if (v.kv_dtype == kBF16)
-        append_kernel<__nv_bfloat16><<<v.B * v.H, kEncThreads, 0, stream>>>(v, layer);
-    else
-        append_kernel<float><<<v.B * v.H, kEncThreads, 0, stream>>>(v, layer);
+    const int hash_ctas = v.retriever == 1 ? v.H * v.words : 0;
+    const size_t sm = hash_ctas ? (size_t)v.d * (64 + kAppendTile) * sizeof(double) : 0;
+    const unsigned grid = (unsigned)(v.B * v.H + hash_ctas);
+    if (v.kv_dtype == kBF16) {
+        cudaFuncSetAttribute(append_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        append_kernel<__nv_bfloat16><<<grid, kEncThreads, sm, stream>>>(v, layer);
+    } else {
+        cudaFuncSetAttribute(append_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        append_kernel<float><<<grid, kEncThreads, sm, stream>>>(v, layer);
+    }
 }
 
 void launch_step_end(const EngineView& v, int* count_a, int* count_b, cudaStream_t stream) {
@@ -257,10 +284,11 @@ void launch_check_finite(const void* p, int dtype, int64_t count, int* err, int 
 }
 
 void launch_window_init(const EngineView& v, cudaStream_t stream) {
-    if (v.kv_dtype == kBF16)
+    if (v.kv_dtype == kBF16) {
         window_init_kernel<__nv_bfloat16><<<v.B * v.L * v.H, 256, 0, stream>>>(v);
-    else
+    } else {
         window_init_kernel<float><<<v.B * v.L * v.H, 256, 0, stream>>>(v);
+    }
 }
 
 }  // namespace clo

@@ -250,6 +250,18 @@ void Engine::allocate() {
             }
         d_proj_t_.alloc(sizeof(double) * pt.size(), false);
         CLO_CUDA(cudaMemcpy(d_proj_t_.p, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice));
+        // the same P^T cut into 64-bit word slices [L*H][words][d][64] (zero past
+        // `bits`): one contiguous bulk copy stages the slice a decode-time hash
+        // CTA needs in shared memory (lookup.cu, encode.cu)
+        std::vector<double> pw((size_t)L * H * words_ * d * 64, 0.0);
+        for (size_t lg = 0; lg < (size_t)L * H; ++lg)
+            for (int w = 0; w < words_; ++w)
+                for (int c = 0; c < d; ++c)
+                    for (int i = 0; i < 64 && w * 64 + i < cfg_.hash_bits; ++i)
+                        pw[((lg * words_ + w) * d + c) * 64 + i] =
+                            pt[(lg * d + c) * cfg_.hash_bits + w * 64 + i];
+        d_proj_w_.alloc(sizeof(double) * pw.size(), false);
+        CLO_CUDA(cudaMemcpy(d_proj_w_.p, pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
     }
     d_labels_.alloc(sizeof(double) * B * L * HQ * d);
     d_label_valid_.alloc(sizeof(int) * B * L * HQ);
@@ -470,6 +482,7 @@ EngineView Engine::view() const {
     v.codes = d_codes_.as<uint64_t>();
     v.code_stride = code_stride_;
     v.proj_t = d_proj_t_.as<double>();
+    v.proj_w = d_proj_w_.as<double>();
     v.labels = d_labels_.as<double>();
     v.label_valid = d_label_valid_.as<int>();
     v.tau = d_tau_.as<double>();
@@ -619,11 +632,7 @@ void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
     ra.layer = layer;
     ra.fresh = fresh;
     prof_begin(st);
-    launch_reconcile(ra, st);
-    if (!fresh && pool_ > cfg_.k) {
-        launch_demote(gather_args(layer, 0), st);  // leaving rows -> victim areas, before the gather
-        launches_ += 1;
-    }
+    launch_reconcile(ra, st);  // demotions travel with the gather's moves
     prof_end(st, "reconcile", layer);
     launches_ += 1;
 }

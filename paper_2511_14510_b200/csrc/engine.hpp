@@ -98,7 +98,7 @@ class Engine {
 
     DevBuf d_persistent_, d_pidx_, d_oidx_, d_tau_, d_qimp_;
     DevBuf d_pk_, d_pv_, d_kmirror_, d_slot_k_, d_slot_v_, d_win_k_, d_win_v_;
-    DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_slot_age_, d_tok2slot_, d_vhead_, d_codes_, d_proj_t_, d_labels_, d_label_valid_;
+    DevBuf d_entry_idx_, d_entry_slot_, d_slot_tok_, d_slot_age_, d_tok2slot_, d_vhead_, d_codes_, d_proj_t_, d_proj_w_, d_labels_, d_label_valid_;
     DevBuf d_hits_, d_misses_, d_cache_last_, d_entry_last_, d_last_hit_, d_history_, d_gathered_;
     DevBuf d_step_, d_desc_, d_err_, d_attn_part_, d_attn_count_, d_xfer_, d_off_layers_;
     int n_off_layers_ = 0;

@@ -25,6 +25,7 @@
 //                   code_stride = nmax*words rounded up to an even word count so
 //                   every segment starts 16-byte aligned (TMA bulk copies)
 //   proj_t          [L*H][d][bits] f64  projection transposed (P^T)
+//   proj_w          [L*H][words][d][64] f64  the same, one contiguous slice per 64-bit code word
 //   labels          [B*L*hq][d] f64, label_valid [B*L*hq]   (QueryLabel)
 //   tau [L*H], qimp [L*H][m]                       (HeadProfileEntry)
 //   seg counters    hits/misses [B*L*H] u64, last_update/entry_last_update,
@@ -107,6 +108,7 @@ struct EngineView {
     uint64_t* codes;
     int64_t code_stride;   // u64 words per segment (even)
     const double* proj_t;
+    const double* proj_w;  // [L*H][words][d][64] f64: P^T in 64-bit word slices (zero past bits)
     double* labels;
     int* label_valid;
     const double* tau;

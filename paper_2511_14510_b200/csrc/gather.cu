@@ -63,15 +63,16 @@ __device__ __forceinline__ int lower_bound(const int32_t* a, int n, int32_t x) {
 //      per head: the slots after the head's cursor (demoted longest ago, or
 //      emptied by promotions) are overwritten first; this step's promotion
 //      sources are skipped.
-// Demotions are copied by demote_kernel (after this kernel, before the
-// gather); promotions and host fetches are the gather kernels' move list. The entry's contents are exactly
+// Demotions, promotions and host fetches are all the gather kernels' move
+// list: a move first copies its slot's leaving row to the victim slot, then
+// stores the incoming row (HBM or PCIe) into the slot. The entry's contents are exactly
 // the reference's (update_entry, similarity_cache.cpp:74-87); only which rows
 // cross PCIe changes.
 //
 // Move list of item i (fetch_*[layer][i][j], j < fetch_count): fetch_slot =
 // destination entry slot; fetch_tok = source token (host row) when >= 0, or
 // -(victim slot + 1) for a promotion; fetch_dem = the victim slot the slot's
-// leaving row is demoted to (demote_kernel), or -1.
+// leaving row is demoted to (by the same move, before the slot is overwritten), or -1.
 __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a) {
     using Scan = cub::BlockScan<int, kRecThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -205,8 +206,8 @@ __global__ void __launch_bounds__(kRecThreads) reconcile_kernel(ReconcileArgs a)
 // Interleaved host K|V (v.kv_fused): one unit covers whole 2*d-element token
 // runs, split into the K and V slots on the way out.
 // Per vector: load the source (host row over PCIe, or the victim slot of a
-// promotion) and store it into the entry slot (its leaving row was demoted by
-// reconcile).
+// promotion) and, when the move demotes, the slot's current vector; store the
+// old vector to its victim slot and the new one into the entry slot.
 __device__ __forceinline__ int gather_units_per_item(const EngineView& v) {
     const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
     if (v.kv_fused) return (v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs;
@@ -239,20 +240,27 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     uint4* pv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * row_bytes);
     const int32_t* ftok = a.fetch_tok + li * v.k;
     const int32_t* fslot = a.fetch_slot + li * v.k;
-    uint4 r[kUnitUnroll];
+    const int32_t* fdem = a.fetch_dem + li * v.k;
+    uint4 r[kUnitUnroll], old[kUnitUnroll];
     uint4* dp[kUnitUnroll];
+    uint4* vp[kUnitUnroll];
     int host = 0;
 #pragma unroll
     for (int uu = 0; uu < kUnitUnroll; ++uu) {
         const int e = v0 + uu * kGatherThreads + threadIdx.x;
+        vp[uu] = nullptr;
         if (e < v1) {
             const int row = e / vpt, c = e - row * vpt;
             // vector c of the moved row: K part (c < vpr) or V part (fused), or matrix `mat`
             const bool isv = fused ? c >= vpr : mat == 1;
             const int cc = fused && isv ? c - vpr : c;
             uint4* pool = isv ? pv : pk;
-            const int slot = fslot[row], src = ftok[row];
+            const int slot = fslot[row], src = ftok[row], dem = fdem[row];
             dp[uu] = pool + (size_t)slot * vpr + cc;
+            if (dem >= 0) {  // the slot's leaving row moves to the victim area first
+                old[uu] = *dp[uu];
+                vp[uu] = pool + (size_t)dem * vpr + cc;
+            }
             if (src >= 0) {
                 r[uu] = hsrc[(size_t)src * rvpr + c];  // PCIe: host row (K|V run when fused)
                 ++host;
@@ -264,57 +272,12 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
 #pragma unroll
     for (int uu = 0; uu < kUnitUnroll; ++uu) {
         const int e = v0 + uu * kGatherThreads + threadIdx.x;
+        if (vp[uu]) *vp[uu] = old[uu];
         if (e < v1) *dp[uu] = r[uu];
     }
     if (a.count_bytes) {
         host = __reduce_add_sync(0xffffffffu, host);
         if ((threadIdx.x & 31) == 0 && host) atomicAdd(v.gathered_bytes, (unsigned long long)host * 16ull);
-    }
-}
-
-// Demotions of one layer (after reconcile, before the gather, on the
-// selection stream): every leaving row the reconcile paired with a victim
-// slot is copied entry slot -> victim slot, 16-byte vectors over the whole
-// grid (HBM -> HBM). Unit = (item, 2 * vpr * kUnitUnroll... vectors).
-__global__ void __launch_bounds__(kGatherThreads) demote_kernel(GatherEngineArgs a) {
-    const EngineView& v = a.v;
-    const int vpr = v.d * dtype_size(v.kv_dtype) / 16;
-    const int per_item = v.k * 2 * vpr;  // vectors if every move demotes
-    const int upi = (per_item + kUnitVecs - 1) / kUnitVecs;
-    const int units = a.count[a.layer] * upi;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int item = u / upi, part = u % upi;
-        const size_t li = (size_t)a.layer * a.items_cap + item;
-        const int n = a.fetch_count[li] * 2 * vpr;
-        const int v0 = part * kUnitVecs;
-        if (v0 >= n) continue;
-        const int seg = a.items[li].seg;
-        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
-        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
-        uint4* pk = reinterpret_cast<uint4*>((char*)v.slot_k + o * v.pool * (size_t)vpr * 16);
-        uint4* pv = reinterpret_cast<uint4*>((char*)v.slot_v + o * v.pool * (size_t)vpr * 16);
-        const int32_t* fslot = a.fetch_slot + li * v.k;
-        const int32_t* fdem = a.fetch_dem + li * v.k;
-        uint4 buf[kUnitUnroll];
-        uint4* to[kUnitUnroll];
-#pragma unroll
-        for (int uu = 0; uu < kUnitUnroll; ++uu) {
-            const int x = v0 + uu * kGatherThreads + threadIdx.x;
-            to[uu] = nullptr;
-            if (x < n) {
-                const int j = x / (2 * vpr), c = x - j * 2 * vpr;
-                const int dem = fdem[j];
-                if (dem >= 0) {
-                    uint4* pool = c < vpr ? pk : pv;
-                    const int cc = c < vpr ? c : c - vpr;
-                    buf[uu] = pool[(size_t)fslot[j] * vpr + cc];
-                    to[uu] = pool + (size_t)dem * vpr + cc;
-                }
-            }
-        }
-#pragma unroll
-        for (int uu = 0; uu < kUnitUnroll; ++uu)
-            if (to[uu]) *to[uu] = buf[uu];
     }
 }
 
@@ -527,10 +490,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     __syncwarp();
     // Row of group i handled by this lane: destination entry slot in its
     // matrix (K, or K then V for fused runs), source = the host row (`host`
-    // set) or the victim slot `prom` of a promotion (the slot's leaving row was
-    // demoted by reconcile already).
+    // set) or the victim slot `prom` of a promotion; `dem` = the victim slot
+    // the slot's leaving row moves to first (or -1).
     struct Row {
-        int rows, mat, slot, prom;
+        int rows, mat, slot, prom, dem;
         size_t o;
         const char* host;
     };
@@ -543,12 +506,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
         const int nf = a.fetch_count[li];
         r.rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
         r.prom = -1;
+        r.dem = -1;
         if (lane < r.rows) {
             const int seg = a.items[li].seg;
             const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
             r.o = (size_t)b * v.NO + v.oidx[l * v.H + g];
             const int j = grp * kTmaRows + lane;
             r.slot = a.fetch_slot[li * v.k + j];
+            r.dem = a.fetch_dem[li * v.k + j];
             const int src = a.fetch_tok[li * v.k + j];
             if (src >= 0) {
                 const size_t base = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
@@ -562,20 +527,36 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     auto row_ptr = [&](int m, size_t o, int slot) {  // pool row `slot` of matrix m
         return (char*)(m ? v.slot_v : v.slot_k) + (o * v.pool + slot) * (size_t)row_bytes;
     };
+    // Leaving rows demoted by this move (reconcile's fetch_dem): the old row
+    // of the entry slot is read into the demotion stage together with the new
+    // row and stored to its victim slot before the new row lands.
+    char* dst0 = tstage + ((size_t)wpc * stages * kTmaRows * cbytes) + (size_t)warp * stages * kTmaRows * cbytes;
     auto load = [&](int i) {
         const Row r = locate(i);
         const int s = i % stages;
         uint64_t* bar = &tbar[warp][s];
+        const int ndem = __popc(__ballot_sync(0xffffffffu, r.dem >= 0));
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (r.rows)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                             "r"(r.rows * cbytes)
+                             "r"((r.rows + ndem) * cbytes)
                              : "memory");
             else
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
         }
         __syncwarp();
+        if (r.dem >= 0) {  // the entry slot's current row(s), HBM
+            const uint32_t dd = smem_u32(dst0 + ((size_t)s * kTmaRows + lane) * cbytes);
+            for (int m = 0; m < (fused ? 2 : 1); ++m) {
+                const int mm = fused ? m : r.mat;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dd + m * row_bytes),
+                    "l"(row_ptr(mm, r.o, r.slot)), "r"(row_bytes), "r"(smem_u32(bar))
+                    : "memory");
+            }
+        }
         if (lane < r.rows) {
             const uint32_t dst = smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes);
             if (r.prom < 0) {  // over PCIe from pinned host memory
@@ -606,6 +587,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
             "@!p bra W_%=;\n\t}" ::"r"(smem_u32(&tbar[warp][s])),
             "r"((i / stages) & 1)
             : "memory");
+        if (r.dem >= 0) {  // demotion first: old row(s) -> victim slot
+            const uint32_t da = smem_u32(dst0 + ((size_t)s * kTmaRows + lane) * cbytes);
+            for (int m = 0; m < (fused ? 2 : 1); ++m)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                 row_ptr(fused ? m : r.mat, r.o, r.dem)),
+                             "r"(da + m * row_bytes), "r"(row_bytes)
+                             : "memory");
+        }
         if (lane < r.rows) {
             const uint32_t sa = smem_u32(st0 + ((size_t)s * kTmaRows + lane) * cbytes);
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
@@ -679,7 +668,7 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
     const int cbytes = v.kv_fused ? 2 * row_bytes : row_bytes;
-    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * cbytes;
+    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * cbytes * (v.pool > v.k ? 2 : 1);  // + demotion stage
     const bool small_region = (int64_t)v.nmax * row_bytes <= (int64_t)48 << 20;  // between the measured 32 / 64 MiB points
     const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
     if (use == 2 && sm <= 200 * 1024) {
@@ -696,14 +685,6 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
                                      : (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
-}
-
-void launch_demote(const GatherEngineArgs& a, cudaStream_t stream) {
-    if (a.v.pool <= a.v.k) return;  // no victim area: nothing is ever demoted
-    const int vpr = a.v.d * dtype_size(a.v.kv_dtype) / 16;
-    const int64_t units = (int64_t)a.items_cap * ((a.v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, 4 * kNumSMs));
-    demote_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 
 void launch_publish(const GatherEngineArgs& a, cudaStream_t stream) { publish_kernel<<<1, 1, 0, stream>>>(a); }

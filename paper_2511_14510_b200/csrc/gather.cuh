@@ -35,9 +35,6 @@ struct GatherEngineArgs {
 };  // items: base of the per-layer work lists [L][items_cap] (gather_unit offsets by layer)
 
 void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream);
-// Demotions of the layer's leaving rows into the victim areas (after
-// reconcile, before the gather); a no-op launch-free call without victim rows.
-void launch_demote(const GatherEngineArgs& a, cudaStream_t stream);
 // Row size must be a multiple of 16 bytes (d*sizeof(dtype) % 16 == 0).
 void launch_gather_engine(const GatherEngineArgs& a, int grid, cudaStream_t stream);
 // GPU-centric transfer pipeline (one decode step): publish(l) after

@@ -1,5 +1,8 @@
 // lookup.cu — K2: device-side similarity-cache decision + work-list build.
+#include <cstdio>
+
 #include "lookup.cuh"
+#include "hash.cuh"
 
 namespace clo {
 
@@ -7,30 +10,49 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 
-// One CTA per (sequence, KV head) of one layer. Decides whether this head's
-// top-k must be (re)selected this step, entirely on the device:
+// One CLUSTER of `words` CTAs per (sequence, KV head) of one layer (one CTA
+// when the retriever is exact). Decides whether this head's top-k must be
+// (re)selected this step, entirely on the device:
 //   persistent heads   always, with the TRUE query (engine.cpp:269-274)
 //   similarity policy  lookup(labels, approx queries, q_importance, tau)
 //                      (engine.cpp:278-320): hit -> reuse the entry;
 //                      miss -> labels := queries (fused, similarity_cache.cpp:63-70)
 //   prefetch_only      always, with the approx query (engine.cpp:340-348)
 //   prefill            every head, step-0 true query (engine.cpp:188-201)
-// Selected heads are appended to the stream's work list with their widened
-// queries and query sign bits.
+// Rank 0 makes the decision and appends a selected head to the stream's work
+// list with its widened queries; it publishes (selected, item) in its shared
+// memory, and every rank r of a selected head then hashes code word r of the
+// m queries against P's word slice staged by one bulk copy (hash.cuh): three
+// dependent memory round trips per head instead of one per batch of P loads.
+#ifdef CLO_PROBE
+__device__ __forceinline__ unsigned __smid_probe() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+#endif
+
 __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     const EngineView& v = a.v;
-    const int b = blockIdx.x / v.H, g = blockIdx.x % v.H, l = a.layer;
+    unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CLO_PROBE_T(tp, 0)
+    const int nr = a.v.retriever == 1 ? v.words : 1;  // cluster size
+    const int rank = (int)(blockIdx.x % nr);
+    const int bg = blockIdx.x / nr;
+    const int b = bg / v.H, g = bg % v.H, l = a.layer;
     const int lg = l * v.H + g;
     const int seg = (b * v.L + l) * v.H + g;
     const bool pers = v.persistent[lg] != 0;
-    if (a.kind == kKindOffloaded && pers) return;
+    if (a.kind == kKindOffloaded && pers) return;  // uniform over the cluster
     if (a.kind == kKindPersistent && !pers) return;
 
-    extern __shared__ double dsm[];  // q [m][d], labels [m][d]
-    double* q = dsm;
-    double* lab_s = dsm + v.m * v.d;
+    extern __shared__ __align__(128) double dsm[];  // P slice [d][64] (hashing), q [m][d], labels [m][d]
+    double* ps = dsm;
+    double* q = dsm + (v.retriever == 1 ? (size_t)v.d * 64 : 0);
+    double* lab_s = q + v.m * v.d;
     __shared__ double sims[kMaxGroup];
     __shared__ int s_degenerate, s_selected, s_item;
+    __shared__ __align__(8) uint64_t bar;
 
     const bool prefill = a.mode == kPrepPrefill;
     const int t = prefill ? 0 : *v.dev_step + 1;
@@ -38,117 +60,153 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     const bool use_true = prefill || pers;
     const float* qsrc = use_true ? v.desc->true_q : v.desc->approx_q;
     const size_t qoff = (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
+    const bool offl_sim = !pers && v.policy == 0;
+    const bool lookup = !prefill && offl_sim && !v.always_hit;
+    double* lab = v.labels + (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
+    int* valid = v.label_valid + ((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m;
+    if (threadIdx.x == 0) {
+        s_selected = 0;
+        s_degenerate = 0;
+        if (nr > 1) bulk::mbar_init(&bar);
+    }
+    // queries (every rank hashes them) and, on rank 0, the labels: one round trip
     for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) {
         const float x = qsrc[qoff + i];
-        if (!isfinite(x)) raise_err(v.err, kErrNonFiniteQuery);
+        if (rank == 0 && !isfinite(x)) raise_err(v.err, kErrNonFiniteQuery);
         q[i] = (double)x;
-    }
-    if (threadIdx.x == 0) s_selected = 0;
-    __syncthreads();
-
-    const bool offl_sim = !pers && v.policy == 0;
-    if (threadIdx.x == 0) {
-        int selected = 0;
-        if (prefill || pers) {
-            selected = 1;
-        } else if (v.policy == 3) {  // prefetch_only
-            selected = 1;
-            v.misses[seg] += 1;
-            v.cache_last_update[seg] = t;
-        } else if (v.always_hit) {  // engine.cpp:280-287
-            v.history[(size_t)seg * v.max_steps + (t - 1)] = 1.0;
-            v.hits[seg] += 1;
-            v.last_lookup_hit[seg] = 1;
-        }
-        s_selected = selected;
+        if (rank == 0 && lookup) lab_s[i] = lab[i];
     }
     __syncthreads();
+    CLO_PROBE_T(tp, 1)
 
-    if (!prefill && offl_sim && !v.always_hit) {
-        // lookup (similarity_cache.cpp:29-72): one thread per group member.
-        double* lab = v.labels + (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
-        int* valid = v.label_valid + ((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m;
-        if (threadIdx.x == 0) s_degenerate = 0;
-        // stage the labels in shared memory: the sequential cosine chains then
-        // read smem instead of paying an L2 round trip per element
-        for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab_s[i] = lab[i];
-        __syncthreads();
-        if (threadIdx.x < v.m) {
-            const int j = threadIdx.x;
-            sims[j] = 0.0;
-            if (valid[j]) {
-                bool deg;
-                const double c = cosine_any(q + j * v.d, lab_s + j * v.d, v.d, &deg);
-                sims[j] = c;
-                if (deg || c <= 0.0) atomicOr(&s_degenerate, 2);
-            } else {
-                atomicOr(&s_degenerate, 1);
-            }
-        }
-        __syncthreads();
+    if (rank == 0) {
         if (threadIdx.x == 0) {
-            const double tau = v.always_miss ? 2.0 : (v.has_tau_override ? v.tau_override : v.tau[lg]);
-            double agg = 0.0;
-            bool hit = false;
-            if (s_degenerate == 0) {  // all valid and all positive
-                agg = aggregate_seq(sims, v.qimp + (size_t)lg * v.m, v.m);
-                hit = agg >= tau;
-            }
-            v.history[(size_t)seg * v.max_steps + (t - 1)] = agg;
-            if (hit) {
-                v.hits[seg] += 1;
-                v.last_lookup_hit[seg] = 1;
-            } else {
-                v.last_lookup_hit[seg] = 0;
+            int selected = 0;
+            if (prefill || pers) {
+                selected = 1;
+            } else if (v.policy == 3) {  // prefetch_only
+                selected = 1;
                 v.misses[seg] += 1;
                 v.cache_last_update[seg] = t;
-                v.entry_last_update[seg] = t;
-                s_selected = 1;
+            } else if (v.always_hit) {  // engine.cpp:280-287
+                v.history[(size_t)seg * v.max_steps + (t - 1)] = 1.0;
+                v.hits[seg] += 1;
+                v.last_lookup_hit[seg] = 1;
+            }
+            s_selected = selected;
+        }
+        if (lookup) {
+            // lookup (similarity_cache.cpp:29-72): one thread per group member,
+            // sequential cosine chains over the staged labels
+            if (threadIdx.x < v.m) {
+                const int j = threadIdx.x;
+                sims[j] = 0.0;
+                if (valid[j]) {
+                    bool deg;
+                    const double c = cosine_any(q + j * v.d, lab_s + j * v.d, v.d, &deg);
+                    sims[j] = c;
+                    if (deg || c <= 0.0) atomicOr(&s_degenerate, 2);
+                } else {
+                    atomicOr(&s_degenerate, 1);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const double tau = v.always_miss ? 2.0 : (v.has_tau_override ? v.tau_override : v.tau[lg]);
+                double agg = 0.0;
+                bool hit = false;
+                if (s_degenerate == 0) {  // all valid and all positive
+                    agg = aggregate_seq(sims, v.qimp + (size_t)lg * v.m, v.m);
+                    hit = agg >= tau;
+                }
+                v.history[(size_t)seg * v.max_steps + (t - 1)] = agg;
+                if (hit) {
+                    v.hits[seg] += 1;
+                    v.last_lookup_hit[seg] = 1;
+                } else {
+                    v.last_lookup_hit[seg] = 0;
+                    v.misses[seg] += 1;
+                    v.cache_last_update[seg] = t;
+                    v.entry_last_update[seg] = t;
+                    s_selected = 1;
+                }
+            }
+            __syncthreads();
+            if (s_selected) {  // fused label refresh on miss
+                for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
+                if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
+            }
+        }
+        if (prefill && offl_sim) {  // engine.cpp:192-200: labels := step-0 true queries
+            for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
+            if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
+            if (threadIdx.x == 0) {
+                v.entry_last_update[seg] = 0;
+                v.cache_last_update[seg] = 0;
             }
         }
         __syncthreads();
-        if (s_selected) {  // fused label refresh on miss
-            for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
-            if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
+        if (s_selected && threadIdx.x == 0) {
+            const int item = atomicAdd(&a.s.count[l], 1);
+            s_item = item;
+            SelItem it;
+            it.seg = seg;
+            it.n = n_pool;
+            const size_t row_bytes = (size_t)v.d * dtype_size(v.kv_dtype);
+            if (pers)
+                it.rows = (const char*)v.pk + ((size_t)b * v.NP + v.pidx[lg]) * v.nmax * row_bytes;
+            else
+                it.rows = v.kmirror ? (const char*)v.kmirror + ((size_t)b * v.NO + v.oidx[lg]) * v.nmax * row_bytes
+                                    : nullptr;
+            it.codes = v.codes ? v.codes + (size_t)seg * v.code_stride : nullptr;
+            // persistent heads select straight into their entry; offloaded heads
+            // select into scratch and are reconciled with the old entry (delta gather)
+            it.out_idx = pers ? v.entry_idx + (size_t)seg * v.k : a.s.sel + (size_t)item * v.k;
+            it.out_score = nullptr;
+            a.s.items[item] = it;
+        }
+        __syncthreads();
+        if (s_selected && v.retriever == 0) {  // the exact retriever scores the widened queries
+            const int item = s_item;
+            for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) a.s.q64[(size_t)item * v.m * v.d + i] = q[i];
         }
     }
-    if (prefill && offl_sim) {  // engine.cpp:192-200: labels := step-0 true queries
-        double* lab = v.labels + (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
-        int* valid = v.label_valid + ((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m;
-        for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
-        if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
-        if (threadIdx.x == 0) {
-            v.entry_last_update[seg] = 0;
-            v.cache_last_update[seg] = 0;
+    CLO_PROBE_T(tp, 2)
+    if (v.retriever != 1) return;
+    int selected = s_selected, item = s_item;
+    if (nr > 1) {
+        // rank 0's decision -> every rank (distributed shared memory)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank != 0) {
+            uint32_t ra, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(bulk::smem_u32(&s_selected)));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(bulk::smem_u32(&s_item)));
+            asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(selected) : "r"(ra) : "memory");
+            asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(item) : "r"(rb) : "memory");
         }
+        // rank 0 stays resident until every rank has read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    if (!s_selected) return;
-
-    if (threadIdx.x == 0) {
-        const int item = atomicAdd(&a.s.count[l], 1);
-        s_item = item;
-        SelItem it;
-        it.seg = seg;
-        it.n = n_pool;
-        const size_t row_bytes = (size_t)v.d * dtype_size(v.kv_dtype);
-        if (pers)
-            it.rows = (const char*)v.pk + ((size_t)b * v.NP + v.pidx[lg]) * v.nmax * row_bytes;
-        else
-            it.rows = v.kmirror ? (const char*)v.kmirror + ((size_t)b * v.NO + v.oidx[lg]) * v.nmax * row_bytes
-                                : nullptr;
-        it.codes = v.codes ? v.codes + (size_t)seg * v.code_stride : nullptr;
-        // persistent heads select straight into their entry; offloaded heads
-        // select into scratch and are reconciled with the old entry (delta gather)
-        it.out_idx = pers ? v.entry_idx + (size_t)seg * v.k : a.s.sel + (size_t)item * v.k;
-        it.out_score = nullptr;
-        a.s.items[item] = it;
+    CLO_PROBE_T(tp, 3)
+    if (!selected) return;
+    // code word `rank` of the m query sign-hashes
+    const double* slice = v.proj_w + ((size_t)lg * v.words + rank) * v.d * 64;
+    if (nr > 1) {
+        if (threadIdx.x == 0) bulk::load_async(ps, slice, (uint32_t)v.d * 64 * 8, &bar);
+        bulk::wait(&bar, 0);
+    } else {
+        for (int i = threadIdx.x; i < v.d * 64; i += blockDim.x) ps[i] = slice[i];
+        __syncthreads();
     }
-    __syncthreads();
-    const int item = s_item;
-    for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) a.s.q64[(size_t)item * v.m * v.d + i] = q[i];
-    if (v.retriever == 1)
-        hash_queries_block(q, v.m, v.d, v.proj_t + (size_t)lg * v.d * v.bits, v.bits, v.words,
-                           a.s.qbits + (size_t)item * v.m * v.words);
+    CLO_PROBE_T(tp, 4)
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(a.s.qbits + (size_t)item * v.m * v.words);
+    hash_word(ps, q, v.d, v.m, v.d, rank, v.bits, [&](int j) { return out32 + (size_t)j * v.words * 2; });
+#ifdef CLO_PROBE
+    CLO_PROBE_T(tp, 5)
+    if (threadIdx.x == 0 && l == 6 && t == 12)
+        printf("PREP %llu b%d g%d r%d sm%u: load %llu decide %llu sync %llu slice %llu hash %llu\n", tp[0], b, g, rank,
+               __smid_probe(), tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4]);
+#endif
 }
 
 // Op-level lookup over independent groups (one warp-sized CTA each).
@@ -235,8 +293,23 @@ __global__ void aggregate_op_kernel(int n, int m, const double* sims, const doub
 }  // namespace
 
 void launch_prepare(const PrepareArgs& a, cudaStream_t stream) {
-    const size_t sm = 2 * (size_t)a.v.m * a.v.d * sizeof(double);
-    prepare_kernel<<<a.v.B * a.v.H, kPrepThreads, sm, stream>>>(a);
+    const int nr = a.v.retriever == 1 ? a.v.words : 1;
+    const size_t sm = (a.v.retriever == 1 ? (size_t)a.v.d * 64 * sizeof(double) : 0) +
+                      2 * (size_t)a.v.m * a.v.d * sizeof(double);
+    cudaFuncSetAttribute(prepare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  // per device
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(a.v.B * a.v.H * nr));
+    cfg.blockDim = dim3(kPrepThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)nr;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, prepare_kernel, a);
 }
 
 void launch_lookup_op(int n_heads, int m, int d, double* labels, int32_t* valid,
