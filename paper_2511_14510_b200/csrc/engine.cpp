@@ -22,6 +22,7 @@
 #include "gather.cuh"
 #include "lookup.cuh"
 #include "select.cuh"
+#include "select_fused.cuh"
 
 namespace clo {
 
@@ -262,6 +263,10 @@ void Engine::allocate() {
                             pt[(lg * d + c) * cfg_.hash_bits + w * 64 + i];
         d_proj_w_.alloc(sizeof(double) * pw.size(), false);
         CLO_CUDA(cudaMemcpy(d_proj_w_.p, pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
+    }
+    if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && words_ <= kMaxHashWords) {
+        fuse_ctl_n_ = L * fused_ctl_stride(B * H);
+        d_fuse_ctl_.alloc(sizeof(int) * fuse_ctl_n_);
     }
     d_labels_.alloc(sizeof(double) * B * L * HQ * d);
     d_label_valid_.alloc(sizeof(int) * B * L * HQ);
@@ -637,6 +642,49 @@ void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
     launches_ += 1;
 }
 
+bool Engine::fused_select() const {
+    static const bool off = [] {  // CLO_FUSED_SELECT=0: the per-stage kernels
+        const char* e = getenv("CLO_FUSED_SELECT");
+        return e && e[0] == '0';
+    }();
+    return !off && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && fuse_ctl_n_ > 0;
+}
+
+void Engine::enqueue_fused_select(int layer, cudaStream_t st) {
+    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
+    FusedSelectArgs f{};
+    f.prep.v = view();
+    f.prep.s = scratch_[1];
+    f.prep.s.items += (size_t)layer * items;
+    f.prep.layer = layer;
+    f.prep.mode = kPrepDecode;
+    f.prep.kind = kKindOffloaded;
+    f.sel = sel_args(1, layer);
+    const SelScratch& sc = scratch_[1];
+    f.rec.v = f.prep.v;
+    f.rec.items = sc.items + (size_t)layer * items;
+    f.rec.count = sc.count;
+    f.rec.sel = sc.sel;
+    f.rec.fetch_tok = sc.fetch_tok;
+    f.rec.fetch_slot = sc.fetch_slot;
+    f.rec.fetch_dem = sc.fetch_dem;
+    f.rec.fetch_count = sc.fetch_count;
+    f.rec.items_cap = (int)items;
+    f.rec.layer = layer;
+    f.rec.fresh = 0;
+    f.ctl = d_fuse_ctl_.as<int>();
+    f.ctl_stride = fused_ctl_stride((int)items);
+    f.items_cap = (int)items;
+    static const int grid = [] {  // CLO_FUSED_GRID: persistent CTAs of the fused selection
+        const char* e = getenv("CLO_FUSED_GRID");
+        return e && atoi(e) > 0 ? atoi(e) : 2 * kNumSMs;
+    }();
+    prof_begin(st);
+    launch_fused_select(f, grid, st);
+    prof_end(st, "select_offloaded", layer);
+    launches_ += 1;
+}
+
 GatherEngineArgs Engine::gather_args(int layer, int count_bytes) const {
     const SelScratch& sc = scratch_[1];
     GatherEngineArgs ga{};
@@ -937,9 +985,13 @@ void Engine::capture_graph(int mode) {
             // it overlaps the compute of layer l-1 (speculative prefetch,
             // engine.cpp:246-251).
             if (l >= 2) CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_attn_[l - 2], 0));
-            enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
-            enqueue_select(1, l, s_pref);
-            enqueue_reconcile(l, 0, s_pref);
+            if (fused_select()) {
+                enqueue_fused_select(l, s_pref);  // lookup .. reconcile in one kernel (select_fused.cu)
+            } else {
+                enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
+                enqueue_select(1, l, s_pref);
+                enqueue_reconcile(l, 0, s_pref);
+            }
             if (!flags) {
                 // one gather launch per layer, ordered by graph edges
                 CLO_CUDA(cudaEventRecord(ev_sel_[l], s_pref));
@@ -985,7 +1037,7 @@ void Engine::capture_graph(int mode) {
         prof_end(s_main_, "exchange_finish", -1);
         launches_ += 2;
     }
-    launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
+    launch_step_end(view(), scratch_[0].count, scratch_[1].count, d_fuse_ctl_.as<int>(), fuse_ctl_n_, s_main_);
     launches_ += 1;
     CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
     capture_mode_ = -1;

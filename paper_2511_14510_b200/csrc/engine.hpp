@@ -67,6 +67,8 @@ class Engine {
     void enqueue_select(int which, int layer, cudaStream_t st);
     void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
     void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
+    void enqueue_fused_select(int layer, cudaStream_t st);
+    bool fused_select() const;
     GatherEngineArgs gather_args(int layer, int count_bytes) const;
     enum GraphMode { kGraphProd = 0, kGraphSerial = 1, kGraphTimeline = 2, kGraphModes = 3 };
     void capture_graph(int mode);
@@ -104,6 +106,8 @@ class Engine {
     int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
     DevBuf d_tmaps_;  // 4 CUtensorMaps over the cache slots (attention TMA boxes)
+    DevBuf d_fuse_ctl_;  // [L][fused_ctl_stride] task counters of the fused selection (select_fused.cuh)
+    int fuse_ctl_n_ = 0;
     // host-input staging, double-buffered: step t+1's H2D copies run on a copy
     // stream while step t's graph still executes
     std::array<DevBuf, 2> d_in_;

@@ -50,137 +50,28 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     double* ps = dsm;
     double* q = dsm + (v.retriever == 1 ? (size_t)v.d * 64 : 0);
     double* lab_s = q + v.m * v.d;
-    __shared__ double sims[kMaxGroup];
-    __shared__ int s_degenerate, s_selected, s_item;
+    __shared__ LookupShared sh;
     __shared__ __align__(8) uint64_t bar;
 
-    const bool prefill = a.mode == kPrepPrefill;
-    const int t = prefill ? 0 : *v.dev_step + 1;
-    const int n_pool = prefill ? v.n_prompt : v.n_prompt + t - 1;
-    const bool use_true = prefill || pers;
-    const float* qsrc = use_true ? v.desc->true_q : v.desc->approx_q;
-    const size_t qoff = (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
-    const bool offl_sim = !pers && v.policy == 0;
-    const bool lookup = !prefill && offl_sim && !v.always_hit;
-    double* lab = v.labels + (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
-    int* valid = v.label_valid + ((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m;
     if (threadIdx.x == 0) {
-        s_selected = 0;
-        s_degenerate = 0;
+        sh.selected = 0;
         if (nr > 1) bulk::mbar_init(&bar);
     }
     // queries (every rank hashes them) and, on rank 0, the labels: one round trip
-    for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) {
-        const float x = qsrc[qoff + i];
-        if (rank == 0 && !isfinite(x)) raise_err(v.err, kErrNonFiniteQuery);
-        q[i] = (double)x;
-        if (rank == 0 && lookup) lab_s[i] = lab[i];
-    }
-    __syncthreads();
+    lookup_stage(a, b, g, rank == 0, q, lab_s);
     CLO_PROBE_T(tp, 1)
 
-    if (rank == 0) {
-        if (threadIdx.x == 0) {
-            int selected = 0;
-            if (prefill || pers) {
-                selected = 1;
-            } else if (v.policy == 3) {  // prefetch_only
-                selected = 1;
-                v.misses[seg] += 1;
-                v.cache_last_update[seg] = t;
-            } else if (v.always_hit) {  // engine.cpp:280-287
-                v.history[(size_t)seg * v.max_steps + (t - 1)] = 1.0;
-                v.hits[seg] += 1;
-                v.last_lookup_hit[seg] = 1;
-            }
-            s_selected = selected;
-        }
-        if (lookup) {
-            // lookup (similarity_cache.cpp:29-72): one thread per group member,
-            // sequential cosine chains over the staged labels
-            if (threadIdx.x < v.m) {
-                const int j = threadIdx.x;
-                sims[j] = 0.0;
-                if (valid[j]) {
-                    bool deg;
-                    const double c = cosine_any(q + j * v.d, lab_s + j * v.d, v.d, &deg);
-                    sims[j] = c;
-                    if (deg || c <= 0.0) atomicOr(&s_degenerate, 2);
-                } else {
-                    atomicOr(&s_degenerate, 1);
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                const double tau = v.always_miss ? 2.0 : (v.has_tau_override ? v.tau_override : v.tau[lg]);
-                double agg = 0.0;
-                bool hit = false;
-                if (s_degenerate == 0) {  // all valid and all positive
-                    agg = aggregate_seq(sims, v.qimp + (size_t)lg * v.m, v.m);
-                    hit = agg >= tau;
-                }
-                v.history[(size_t)seg * v.max_steps + (t - 1)] = agg;
-                if (hit) {
-                    v.hits[seg] += 1;
-                    v.last_lookup_hit[seg] = 1;
-                } else {
-                    v.last_lookup_hit[seg] = 0;
-                    v.misses[seg] += 1;
-                    v.cache_last_update[seg] = t;
-                    v.entry_last_update[seg] = t;
-                    s_selected = 1;
-                }
-            }
-            __syncthreads();
-            if (s_selected) {  // fused label refresh on miss
-                for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
-                if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
-            }
-        }
-        if (prefill && offl_sim) {  // engine.cpp:192-200: labels := step-0 true queries
-            for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) lab[i] = q[i];
-            if (threadIdx.x < v.m) valid[threadIdx.x] = 1;
-            if (threadIdx.x == 0) {
-                v.entry_last_update[seg] = 0;
-                v.cache_last_update[seg] = 0;
-            }
-        }
-        __syncthreads();
-        if (s_selected && threadIdx.x == 0) {
-            const int item = atomicAdd(&a.s.count[l], 1);
-            s_item = item;
-            SelItem it;
-            it.seg = seg;
-            it.n = n_pool;
-            const size_t row_bytes = (size_t)v.d * dtype_size(v.kv_dtype);
-            if (pers)
-                it.rows = (const char*)v.pk + ((size_t)b * v.NP + v.pidx[lg]) * v.nmax * row_bytes;
-            else
-                it.rows = v.kmirror ? (const char*)v.kmirror + ((size_t)b * v.NO + v.oidx[lg]) * v.nmax * row_bytes
-                                    : nullptr;
-            it.codes = v.codes ? v.codes + (size_t)seg * v.code_stride : nullptr;
-            // persistent heads select straight into their entry; offloaded heads
-            // select into scratch and are reconciled with the old entry (delta gather)
-            it.out_idx = pers ? v.entry_idx + (size_t)seg * v.k : a.s.sel + (size_t)item * v.k;
-            it.out_score = nullptr;
-            a.s.items[item] = it;
-        }
-        __syncthreads();
-        if (s_selected && v.retriever == 0) {  // the exact retriever scores the widened queries
-            const int item = s_item;
-            for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) a.s.q64[(size_t)item * v.m * v.d + i] = q[i];
-        }
-    }
+    if (rank == 0) lookup_decide(a, b, g, q, lab_s, sh);
     CLO_PROBE_T(tp, 2)
     if (v.retriever != 1) return;
-    int selected = s_selected, item = s_item;
+    int selected = sh.selected, item = sh.item;
     if (nr > 1) {
         // rank 0's decision -> every rank (distributed shared memory)
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (rank != 0) {
             uint32_t ra, rb;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(bulk::smem_u32(&s_selected)));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(bulk::smem_u32(&s_item)));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(bulk::smem_u32(&sh.selected)));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(bulk::smem_u32(&sh.item)));
             asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(selected) : "r"(ra) : "memory");
             asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(item) : "r"(rb) : "memory");
         }

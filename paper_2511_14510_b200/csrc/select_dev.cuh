@@ -1,0 +1,197 @@
+// select_dev.cuh — CTA-wide device functions of the sign-hash selection
+// (threshold of one item, compaction of one chunk), shared by the per-stage
+// kernels in select.cu and the fused per-layer selection kernel.
+#pragma once
+
+#include "select.cuh"
+
+namespace clo {
+
+__device__ __forceinline__ int num_chunks(int n) { return (n + kScoreChunk - 1) / kScoreChunk; }
+
+// Per item: T = k-th largest S (ties resolved later by index), then each
+// chunk's output offset and how many of its S == T ties it keeps.
+// Whole CTA; smem = nb + 2*max_chunks words, sts = 2 ints. Ends with __syncthreads().
+__device__ __forceinline__ void threshold_item(const SelArgs& a, int item, uint32_t* smem, int* sts) {
+    uint32_t* tot = smem;                               // [nb]
+    int* gt = reinterpret_cast<int*>(smem + a.nb);      // [max_chunks]
+    int* eq = gt + a.max_chunks;                        // [max_chunks]
+    int& sT = sts[0];
+    int& sGt = sts[1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    {
+        const SelItem it = a.items[item];
+        const int nch = num_chunks(it.n);
+        const uint32_t* hist = a.chunk_hist + (size_t)item * a.max_chunks * a.nb;
+        if (nch <= 64) {  // one thread per bin walks the chunks
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
+                uint32_t s = 0;
+#pragma unroll 8
+                for (int c = 0; c < nch; ++c) s += hist[(size_t)c * a.nb + b];
+                tot[b] = s;
+            }
+        } else {  // long items: warp w sums chunks w, w + nwarps, ... (coalesced bin rows)
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
+            __syncthreads();
+            for (int b0 = 0; b0 < a.nb; b0 += 32) {
+                const int b = b0 + lane;
+                if (b < a.nb) {
+                    uint32_t s = 0;
+#pragma unroll 4
+                    for (int c = warp; c < nch; c += nwarps) s += hist[(size_t)c * a.nb + b];
+                    if (s) atomicAdd(&tot[b], s);
+                }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // Walk bins from the top in blocks of 32: suffix sums by warp scan.
+            int running = 0, T = -1, gtT = 0;
+            for (int top = a.nb - 1; top >= 0 && T < 0; top -= 32) {
+                const int b = top - lane;
+                int v = b >= 0 ? (int)tot[b] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= a.k);
+                if (hit) {
+                    const int first = __ffs(hit) - 1;
+                    const int excl = __shfl_sync(0xffffffffu, incl - v, first);
+                    T = top - first;
+                    gtT = running + excl;
+                }
+                running += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) {
+                sT = T;
+                sGt = gtT;
+            }
+        }
+        __syncthreads();
+        const int T = sT, need_eq = a.k - sGt;
+        for (int c = warp; c < nch; c += nwarps) {
+            const uint32_t* h = hist + (size_t)c * a.nb;
+            int g = 0;
+            for (int b = T + 1 + lane; b < a.nb; b += 32) g += h[b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+            if (lane == 0) {
+                gt[c] = g;
+                eq[c] = h[T];
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int base_run = 0, eq_run = 0;
+            for (int c0 = 0; c0 < nch; c0 += 32) {
+                const int c = c0 + lane;
+                const int e = c < nch ? eq[c] : 0;
+                int ie = e;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, ie, o);
+                    if (lane >= o) ie += t;
+                }
+                const int eq_before = eq_run + ie - e;
+                const int take = max(0, min(e, need_eq - eq_before));
+                const int contrib = c < nch ? gt[c] + take : 0;
+                int ic = contrib;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, ic, o);
+                    if (lane >= o) ic += t;
+                }
+                if (c < nch) {
+                    a.chunk_base[(size_t)item * a.max_chunks + c] = base_run + ic - contrib;
+                    a.chunk_take[(size_t)item * a.max_chunks + c] = take;
+                }
+                base_run += __shfl_sync(0xffffffffu, ic, 31);
+                eq_run += __shfl_sync(0xffffffffu, ie, 31);
+            }
+            if (lane == 0) {
+                a.thresh[item] = (uint64_t)T;
+                a.need[item] = need_eq;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <typename KeyT>
+__device__ __forceinline__ double key_score(KeyT k);
+template <>
+__device__ __forceinline__ double key_score<uint16_t>(uint16_t k) { return (double)k; }
+template <>
+__device__ __forceinline__ double key_score<uint64_t>(uint64_t k) { return key_to_double(k); }
+
+// Keeps S > T and the first chunk_take ties S == T (index order) of one chunk,
+// writing indices ascending at chunk_base (select_topk's final ascending sort,
+// retrieval.cpp:43, merge_group_topk's :197-199). Warp w owns 512 consecutive
+// rows: pass 1 counts (coalesced key loads), a tiny 8-warp prefix in shared
+// memory orders the warps, pass 2 re-reads the keys (L1) and emits with
+// ballot/popc ranks — two barriers per chunk, no block-wide scans.
+// One (item, chunk) unit, kScoreThreads threads; s_gt/s_eq = kScoreThreads/32
+// ints each. Ends with __syncthreads() (when the chunk exists).
+template <typename KeyT>
+__device__ __forceinline__ void compact_unit(const SelArgs& a, int item, int chunk, int* s_gt, int* s_eq) {
+    constexpr int kW = kScoreThreads / 32;
+    constexpr int kRowsPerWarp = kScoreChunk / kW;  // 512
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    {
+        const SelItem it = a.items[item];
+        const int start = chunk * kScoreChunk;
+        if (start >= it.n) return;
+        const int end = min(start + kScoreChunk, it.n);
+        const KeyT T = (KeyT)a.thresh[item];
+        const int take = a.chunk_take[(size_t)item * a.max_chunks + chunk];
+        const int base = a.chunk_base[(size_t)item * a.max_chunks + chunk];
+        const KeyT* keys = (sizeof(KeyT) == 2 ? (const KeyT*)(a.key16 + (size_t)item * a.nmax)
+                                              : (const KeyT*)(a.key64 + (size_t)item * a.nmax));
+        const int w0 = start + warp * kRowsPerWarp, w1 = min(w0 + kRowsPerWarp, end);
+        int gt = 0, eq = 0;
+        for (int r = w0 + lane; r < w1; r += 32) {
+            const KeyT kv = keys[r];
+            gt += kv > T;
+            eq += kv == T;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            gt += __shfl_xor_sync(0xffffffffu, gt, o);
+            eq += __shfl_xor_sync(0xffffffffu, eq, o);
+        }
+        if (lane == 0) {
+            s_gt[warp] = gt;
+            s_eq[warp] = eq;
+        }
+        __syncthreads();
+        int eq_before = 0, pos = base;
+        for (int w = 0; w < warp; ++w) {
+            pos += s_gt[w] + max(0, min(s_eq[w], take - eq_before));
+            eq_before += s_eq[w];
+        }
+        for (int r0 = w0; r0 < w1; r0 += 32) {
+            const int r = r0 + lane;
+            const bool valid = r < w1;
+            const KeyT kv = valid ? keys[r] : (KeyT)0;
+            const bool is_eq = valid && kv == T;
+            const unsigned eqm = __ballot_sync(0xffffffffu, is_eq);
+            const bool sel = (valid && kv > T) || (is_eq && eq_before + __popc(eqm & lt) < take);
+            const unsigned selm = __ballot_sync(0xffffffffu, sel);
+            if (sel) {
+                const int p = pos + __popc(selm & lt);
+                it.out_idx[p] = r;
+                if (it.out_score) it.out_score[p] = key_score<KeyT>(kv);
+            }
+            pos += __popc(selm);
+            eq_before += __popc(eqm);
+        }
+        __syncthreads();
+    }
+}
+
+
+}  // namespace clo
