@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kEncThreads) append_kernel(EngineView v, int l
     }
 }
 
-__global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L, int* claim, int* done, int* ctl, int nctl) {
+__global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L, int* claim, int* done) {
     if (threadIdx.x == 0) *dev_step += 1;
     for (int i = threadIdx.x; i < L; i += blockDim.x) {
         ca[i] = 0;
@@ -182,7 +182,6 @@ __global__ void step_end_kernel(int* dev_step, int* ca, int* cb, int L, int* cla
         if (claim) claim[i] = 0;
         if (done) done[i] = 0;
     }
-    for (int i = threadIdx.x; i < nctl; i += blockDim.x) ctl[i] = 0;  // fused selection task counters
 }
 
 template <typename T>
@@ -262,8 +261,8 @@ void launch_append(const EngineView& v, int layer, cudaStream_t stream) {
     }
 }
 
-void launch_step_end(const EngineView& v, int* count_a, int* count_b, int* ctl, int nctl, cudaStream_t stream) {
-    step_end_kernel<<<1, 256, 0, stream>>>(v.dev_step, count_a, count_b, v.L, v.xfer_claim, v.xfer_done, ctl, nctl);
+void launch_step_end(const EngineView& v, int* count_a, int* count_b, cudaStream_t stream) {
+    step_end_kernel<<<1, 128, 0, stream>>>(v.dev_step, count_a, count_b, v.L, v.xfer_claim, v.xfer_done);
 }
 
 void launch_check_finite(const void* p, int dtype, int64_t count, int* err, int bit,

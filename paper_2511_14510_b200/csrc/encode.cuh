@@ -29,7 +29,7 @@ void launch_append(const EngineView& v, int layer, cudaStream_t stream);
 
 // Marks the step complete (device step counter) and clears the per-layer
 // work-list counters for the next step.
-void launch_step_end(const EngineView& v, int* count_a, int* count_b, int* ctl, int nctl, cudaStream_t stream);
+void launch_step_end(const EngineView& v, int* count_a, int* count_b, cudaStream_t stream);
 
 // Scans n*d values for non-finite entries (check_qkv, attention.cpp:11-23).
 void launch_check_finite(const void* p, int dtype, int64_t count, int* err, int bit,

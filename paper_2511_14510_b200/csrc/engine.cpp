@@ -264,10 +264,6 @@ void Engine::allocate() {
         d_proj_w_.alloc(sizeof(double) * pw.size(), false);
         CLO_CUDA(cudaMemcpy(d_proj_w_.p, pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
     }
-    if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && words_ <= kMaxHashWords) {
-        fuse_ctl_n_ = L * fused_ctl_stride(B * H);
-        d_fuse_ctl_.alloc(sizeof(int) * fuse_ctl_n_);
-    }
     d_labels_.alloc(sizeof(double) * B * L * HQ * d);
     d_label_valid_.alloc(sizeof(int) * B * L * HQ);
     d_hits_.alloc(sizeof(unsigned long long) * segs);
@@ -365,6 +361,7 @@ void Engine::allocate() {
         bufs[9].alloc(sizeof(uint64_t) * items);
         bufs[10].alloc(sizeof(int) * items);
         bufs[11].alloc(sizeof(uint32_t) * items * 256);
+        bufs[17].alloc(sizeof(int) * 2 * items);  // chained-stage chunk counters (zero between launches)
         if (i == 1) {  // offloaded heads: new selections + per-layer fetch lists
             bufs[12].alloc(sizeof(int32_t) * items * k, false);
             bufs[13].alloc(sizeof(int32_t) * L * items * k, false);
@@ -389,6 +386,7 @@ void Engine::allocate() {
         sc.fetch_slot = bufs[14].as<int32_t>();
         sc.fetch_count = bufs[15].as<int>();
         sc.fetch_dem = bufs[16].as<int32_t>();
+        sc.item_done = bufs[17].as<int>();
     }
 
     CLO_CUDA(cudaStreamCreateWithFlags(&s_main_, cudaStreamNonBlocking));
@@ -561,6 +559,7 @@ SelArgs Engine::sel_args(int which, int layer) const {
     a.radix_hist = sc.radix_hist;
     a.grid = grid_for((int64_t)cfg_.batch * s.num_kv_heads * max_chunks_);
     a.max_items = cfg_.batch * s.num_kv_heads;
+    a.item_done = chained_select() ? sc.item_done : nullptr;
     return a;
 }
 
@@ -594,12 +593,41 @@ void Engine::drop_graphs() {  // views and pointers are baked into the graphs
     }
 }
 
-void Engine::enqueue_select(int which, int layer, cudaStream_t st) {
+bool Engine::chained_select() const {
+    static const bool off = [] {  // CLO_CHAIN_SELECT=0: separate threshold and reconcile launches
+        const char* e = getenv("CLO_CHAIN_SELECT");
+        return e && e[0] == '0';
+    }();
+    return !off && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && (size_t)cfg_.k * 16 <= 200 * 1024;
+}
+
+ReconcileArgs Engine::reconcile_args(int layer, int fresh) const {
+    const SelScratch& sc = scratch_[1];
+    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
+    ReconcileArgs ra{};
+    ra.v = view();
+    ra.items = sc.items + (size_t)layer * items;
+    ra.count = sc.count;
+    ra.sel = sc.sel;
+    ra.fetch_tok = sc.fetch_tok;
+    ra.fetch_slot = sc.fetch_slot;
+    ra.fetch_dem = sc.fetch_dem;
+    ra.fetch_count = sc.fetch_count;
+    ra.items_cap = (int)items;
+    ra.layer = layer;
+    ra.fresh = fresh;
+    return ra;
+}
+
+void Engine::enqueue_select(int which, int layer, cudaStream_t st, bool with_reconcile) {
     SelArgs a = sel_args(which, layer);
     prof_begin(st);
     if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH) {
-        launch_select_signhash(a, st);
-        launches_ += 3;
+        // decode, offloaded heads, chained stages: the compaction kernel also
+        // reconciles each item's entry (one launch instead of two)
+        const ReconcileArgs ra = reconcile_args(layer, 0);
+        launch_select_signhash(a, st, with_reconcile && a.item_done ? &ra : nullptr);
+        launches_ += a.item_done ? 2 : 3;
     } else {
         launch_select_exact(a, st);
         launches_ += 21;
@@ -622,20 +650,7 @@ void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStrea
 }
 
 void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
-    const SelScratch& sc = scratch_[1];
-    const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
-    ReconcileArgs ra{};
-    ra.v = view();
-    ra.items = sc.items + (size_t)layer * items;
-    ra.count = sc.count;
-    ra.sel = sc.sel;
-    ra.fetch_tok = sc.fetch_tok;
-    ra.fetch_slot = sc.fetch_slot;
-    ra.fetch_dem = sc.fetch_dem;
-    ra.fetch_count = sc.fetch_count;
-    ra.items_cap = (int)items;
-    ra.layer = layer;
-    ra.fresh = fresh;
+    const ReconcileArgs ra = reconcile_args(layer, fresh);
     prof_begin(st);
     launch_reconcile(ra, st);  // demotions travel with the gather's moves
     prof_end(st, "reconcile", layer);
@@ -643,11 +658,13 @@ void Engine::enqueue_reconcile(int layer, int fresh, cudaStream_t st) {
 }
 
 bool Engine::fused_select() const {
-    static const bool off = [] {  // CLO_FUSED_SELECT=0: the per-stage kernels
+    static const bool off = [] {  // CLO_FUSED_SELECT=1: one cluster kernel per layer (experiment; slower on B200)
         const char* e = getenv("CLO_FUSED_SELECT");
-        return e && e[0] == '0';
+        return !(e && e[0] == '1');
     }();
-    return !off && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && fuse_ctl_n_ > 0;
+    return !off && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH &&
+           fused_select_fits(words_, nb_, cfg_.shape.num_q_heads / cfg_.shape.num_kv_heads, cfg_.shape.head_dim, cfg_.k,
+                             nmax_);
 }
 
 void Engine::enqueue_fused_select(int layer, cudaStream_t st) {
@@ -672,15 +689,8 @@ void Engine::enqueue_fused_select(int layer, cudaStream_t st) {
     f.rec.items_cap = (int)items;
     f.rec.layer = layer;
     f.rec.fresh = 0;
-    f.ctl = d_fuse_ctl_.as<int>();
-    f.ctl_stride = fused_ctl_stride((int)items);
-    f.items_cap = (int)items;
-    static const int grid = [] {  // CLO_FUSED_GRID: persistent CTAs of the fused selection
-        const char* e = getenv("CLO_FUSED_GRID");
-        return e && atoi(e) > 0 ? atoi(e) : 2 * kNumSMs;
-    }();
     prof_begin(st);
-    launch_fused_select(f, grid, st);
+    launch_fused_select(f, st);
     prof_end(st, "select_offloaded", layer);
     launches_ += 1;
 }
@@ -989,8 +999,8 @@ void Engine::capture_graph(int mode) {
                 enqueue_fused_select(l, s_pref);  // lookup .. reconcile in one kernel (select_fused.cu)
             } else {
                 enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
-                enqueue_select(1, l, s_pref);
-                enqueue_reconcile(l, 0, s_pref);
+                enqueue_select(1, l, s_pref, true);
+                if (!chained_select()) enqueue_reconcile(l, 0, s_pref);
             }
             if (!flags) {
                 // one gather launch per layer, ordered by graph edges
@@ -1037,7 +1047,7 @@ void Engine::capture_graph(int mode) {
         prof_end(s_main_, "exchange_finish", -1);
         launches_ += 2;
     }
-    launch_step_end(view(), scratch_[0].count, scratch_[1].count, d_fuse_ctl_.as<int>(), fuse_ctl_n_, s_main_);
+    launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
     CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
     capture_mode_ = -1;

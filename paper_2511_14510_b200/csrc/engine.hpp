@@ -64,7 +64,9 @@ class Engine {
     EngineView view() const;
     SelArgs sel_args(int which, int layer) const;
     void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
-    void enqueue_select(int which, int layer, cudaStream_t st);
+    void enqueue_select(int which, int layer, cudaStream_t st, bool with_reconcile = false);
+    bool chained_select() const;
+    ReconcileArgs reconcile_args(int layer, int fresh) const;
     void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
     void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
     void enqueue_fused_select(int layer, cudaStream_t st);
@@ -106,8 +108,6 @@ class Engine {
     int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
     DevBuf d_tmaps_;  // 4 CUtensorMaps over the cache slots (attention TMA boxes)
-    DevBuf d_fuse_ctl_;  // [L][fused_ctl_stride] task counters of the fused selection (select_fused.cuh)
-    int fuse_ctl_n_ = 0;
     // host-input staging, double-buffered: step t+1's H2D copies run on a copy
     // stream while step t's graph still executes
     std::array<DevBuf, 2> d_in_;
@@ -117,7 +117,7 @@ class Engine {
     std::array<bool, 2> in_used_{};
     int pending_free_ = -1;  // slot whose consumer graph is being launched
     std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
-    std::array<std::array<DevBuf, 17>, 2> scratch_bufs_;
+    std::array<std::array<DevBuf, 18>, 2> scratch_bufs_;
 
     cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_xfer_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr;

@@ -68,6 +68,7 @@ struct SelScratch {
     int32_t* fetch_slot;   // [L][B*H][k]   destination entry slot
     int32_t* fetch_dem;    // [L][B*H][k]   victim slot the leaving row moves to first, or -1
     int* fetch_count;      // [L][B*H]
+    int* item_done;        // [2][B*H] chunk counters of the chained score/threshold and compact/reconcile
 };
 
 struct EngineView {

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     hash_word(ps, q, v.d, v.m, v.d, rank, v.bits, [&](int j) { return out32 + (size_t)j * v.words * 2; });
 #ifdef CLO_PROBE
     CLO_PROBE_T(tp, 5)
-    if (threadIdx.x == 0 && l == 6 && t == 12)
+    if (threadIdx.x == 0 && l == 6 && *v.dev_step + 1 == 12)
         printf("PREP %llu b%d g%d r%d sm%u: load %llu decide %llu sync %llu slice %llu hash %llu\n", tp[0], b, g, rank,
                __smid_probe(), tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4]);
 #endif

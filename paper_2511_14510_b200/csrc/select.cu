@@ -7,6 +7,7 @@
 
 #include "select.cuh"
 #include "select_dev.cuh"
+#include "reconcile.cuh"
 
 namespace clo {
 
@@ -100,7 +101,9 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
     uint32_t* whist = reinterpret_cast<uint32_t*>(sm + 2 * kPieceRows * W * 8);     // [kWarps][nb]
     uint64_t* qb = reinterpret_cast<uint64_t*>(sm + 2 * kPieceRows * W * 8 +
                                                ((size_t)kWarps * a.nb * 4 + 7) / 8 * 8);  // [m][W]
+    uint32_t* thr_sm = reinterpret_cast<uint32_t*>(qb + a.m * W);                        // threshold_item's
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int s_last, s_sts[2];
     const int units = *a.count * a.max_chunks;
     const int mine = units > (int)blockIdx.x ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = mine * kPieces;
@@ -202,6 +205,20 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
                 out[b] = sum;
             }
             __syncthreads();
+            // the CTA finishing the item's last chunk computes its threshold
+            // (threshold_signhash_kernel's work, without another launch)
+            const int nch = num_chunks(a.items[item].n);
+            if (a.item_done && chunk < nch) {
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) s_last = atomicAdd(&a.item_done[item], 1) == nch - 1;
+                __syncthreads();
+                if (s_last) {
+                    __threadfence();
+                    threshold_item(a, item, thr_sm, s_sts);
+                    if (threadIdx.x == 0) a.item_done[item] = 0;  // ready for the next layer
+                }
+            }
         }
     }
 }
@@ -222,6 +239,32 @@ __global__ void __launch_bounds__(kScoreThreads) compact_kernel(SelArgs a) {
     __shared__ int s_gt[kWarps], s_eq[kWarps];
     const int units = *a.count * a.max_chunks;
     for (int u = blockIdx.x; u < units; u += gridDim.x) compact_unit<KeyT>(a, u / a.max_chunks, u % a.max_chunks, s_gt, s_eq);
+}
+
+// Compaction of the offloaded heads whose CTA finishing an item's last chunk
+// then reconciles that item's entry (reconcile_kernel's work, reconcile.cuh):
+// the fetch list is ready when this kernel ends, one launch earlier.
+__global__ void __launch_bounds__(kScoreThreads) compact_reconcile_kernel(SelArgs a, ReconcileArgs r) {
+    __shared__ int s_gt[kWarps], s_eq[kWarps], s_last;
+    __shared__ ReconcileSmem<kScoreThreads> rsm;
+    extern __shared__ int32_t rs[];  // [4][k]
+    int* done = a.item_done + a.max_items;
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const int nch = num_chunks(a.items[item].n);
+        if (chunk >= nch) continue;
+        compact_unit<uint16_t>(a, item, chunk, s_gt, s_eq);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&done[item], 1) == nch - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            reconcile_item<kScoreThreads>(r, item, rs, rsm);
+            if (threadIdx.x == 0) done[item] = 0;
+        }
+    }
 }
 
 // -------------------------------------------------------------------- exact
@@ -410,14 +453,14 @@ __global__ void chunk_prefix_kernel(SelArgs a) {
 
 }  // namespace
 
-void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
+void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec) {
     const size_t sm_score = (size_t)kWarps * a.nb * 4 + 8 + (size_t)a.m * a.words * 8;
     static const bool tma = [] {  // CLO_SCORE=lsu: the register-load kernel
         const char* e = getenv("CLO_SCORE");
         return !(e && std::string(e) == "lsu");
     }();
     const size_t sm_tma = 2 * (size_t)kPieceRows * a.words * 8 + ((size_t)kWarps * a.nb * 4 + 7) / 8 * 8 +
-                          (size_t)a.m * a.words * 8;
+                          (size_t)a.m * a.words * 8 + ((size_t)a.nb + 2 * (size_t)a.max_chunks) * 4;
     static const int grid_cap = [] {  // CLO_SCORE_GRID: experiment switch
         const char* e = getenv("CLO_SCORE_GRID");
         return e && atoi(e) > 0 ? atoi(e) : 8 * kNumSMs;  // measured: more CTAs than resident slots balance the chunks
@@ -446,8 +489,15 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream) {
     const size_t sm_thr = (size_t)a.nb * 4 + (size_t)a.max_chunks * 8;
     // one CTA per item (the kernels grid-stride over *count <= max_items)
     const int items_grid = a.max_items > 0 ? (a.max_items < 1024 ? a.max_items : 1024) : (a.grid < 1024 ? a.grid : 1024);
-    threshold_signhash_kernel<<<items_grid, 1024, sm_thr, stream>>>(a);
-    compact_kernel<uint16_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
+    const bool tma_chained = tma && a.item_done;  // the score kernel's last chunk per item ran the threshold
+    if (!tma_chained) threshold_signhash_kernel<<<items_grid, 1024, sm_thr, stream>>>(a);
+    if (rec && a.item_done) {
+        const size_t sm_rec = 4 * sizeof(int32_t) * (size_t)a.k;
+        cudaFuncSetAttribute(compact_reconcile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rec);
+        compact_reconcile_kernel<<<a.grid, kScoreThreads, sm_rec, stream>>>(a, *rec);
+    } else {
+        compact_kernel<uint16_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
+    }
 }
 
 void launch_select_exact(const SelArgs& a, cudaStream_t stream) {

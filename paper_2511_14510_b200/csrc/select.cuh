@@ -46,10 +46,16 @@ struct SelArgs {
     uint32_t* radix_hist;   // [item][256]
     int grid;               // CTAs for the grid-stride kernels
     int max_items;          // host-side upper bound of *count (sizes the per-item grids)
+    int* item_done;         // [2][max_items] zeroed chunk counters, or null: the CTA finishing an item's
+                            // last score chunk computes its threshold, the one finishing its last
+                            // compaction chunk reconciles it (no separate threshold / reconcile launch)
 };
 
 // Host launchers (select.cu). All enqueue on `stream`; no host sync.
-void launch_select_signhash(const SelArgs& a, cudaStream_t stream);
+struct ReconcileArgs;
+// rec: offloaded heads in a decode step — the compaction kernel also reconciles
+// their entries (needs a.item_done); null: compaction only
+void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec = nullptr);
 void launch_select_exact(const SelArgs& a, cudaStream_t stream);
 // Query sign bits for op-level calls (one CTA): q64 [m][d] -> qbits [m][words].
 void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, int bits,

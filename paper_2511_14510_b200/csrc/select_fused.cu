@@ -1,274 +1,414 @@
 // select_fused.cu — the whole selection of one decode layer (offloaded heads,
-// sign-hash retriever) as ONE kernel: lookup + query hash, scoring,
-// threshold, compaction and the entry reconcile.
+// sign-hash retriever) in ONE kernel: lookup + query hash, scoring,
+// threshold, compaction and the entry reconcile, one thread-block CLUSTER of
+// CS CTAs per (sequence, KV head).
 //
-// Why one kernel: while the zero-copy gather of the previous layer keeps the
-// PCIe link busy, every kernel boundary on another stream waits for the
-// memory system to drain the queued host reads — measured on B200 at 9 us
-// (32 one-warp gather CTAs) to 40 us (128) per graph edge instead of 0.4 us
+// Why: while the zero-copy gather keeps host reads queued in the memory
+// system, every global synchronisation — a kernel boundary, a
+// __threadfence() — waits behind that queue: measured on B200 beside a
+// saturating gather, a graph edge between two empty kernels costs 9 us (32
+// one-warp gather CTAs) to 40 us (128) instead of 0.4 us
 // (tools/boundary_probe.cu, profiles/README.md round 2). The per-stage chain
-// (prepare -> score -> threshold -> compact -> reconcile) paid that five
-// times per layer and became the step's critical path: the transfer stream
-// sat idle ~22% of the step waiting for fetch lists. Here the stages are
-// tasks of one persistent grid, claimed in order from a per-layer counter:
+// (prepare -> score -> threshold -> compact -> reconcile) paid that five times
+// per layer and was the step's critical path (the transfer stream idled ~22%
+// of the step waiting for fetch lists); a task-queue version synchronised
+// through global counters paid it per task. Here a missed head is handled
+// start to finish by its own cluster, whose ranks synchronise with the
+// hardware cluster barrier and exchange through distributed shared memory:
 //
-//   [0, B*H)               lookup of (sequence, KV head) p: the similarity
-//                          decision (lookup_decide, lookup.cuh); on a miss the
-//                          head becomes work item `item` and the CTA hashes
-//                          the m approximate queries, one P^T word slice at a
-//                          time from shared memory (hash.cuh)
-//   then C*NC score tasks  (item, 4096-row chunk): S(i) and the chunk
-//                          histogram; the CTA finishing an item's last chunk
-//                          computes its threshold (threshold_item)
-//   then C*NC compaction   (item, chunk) after the item's threshold; the CTA
-//   tasks                  finishing an item's last chunk reconciles the entry
-//                          (reconcile_item) and publishes its fetch list
+//   rank 0     lookup_decide (lookup.cuh): the similarity decision, label
+//              refresh and work-list entry; the decision reaches the other
+//              ranks through DSMEM. Hits end here.
+//   rank r     hashes code words r, r+CS, ... of the m approximate queries
+//              against P's word slices staged by bulk copies (hash.cuh); the
+//              words are exchanged through DSMEM
+//   rank r     scores rows [r*n/CS, (r+1)*n/CS) (codes streamed by
+//              cp.async.bulk through a 2-stage ring), writes the u16 keys and
+//              its histogram of S
+//   every rank sums the CS histograms (DSMEM) -> T = k-th largest S and the
+//              number of S == T ties to keep; counts its rows > T and == T;
+//              the counts give each rank its output offset and tie quota
+//              (ties go by ascending index = rank order), and it writes its
+//              part of the ascending selection
+//   rank 0     reconciles the entry (reconcile.cuh): the layer's fetch list
 //
-// C (missed heads) is known once every lookup task is done; later tasks wait
-// for that. A task only ever waits for tasks claimed before it, and a claimed
-// task belongs to a running CTA, so the grid makes progress whatever the
-// residency. Counters live in a per-layer control block (reset at step end).
-// Results are identical to the per-stage kernels (same device functions).
+// The result is the per-stage kernels' result bit for bit: the top-k of
+// S(i) = max_j score_j(i) under (S desc, i asc), ascending
+// (retrieval.cpp:33-46, :90-125; similarity_cache.cpp:180-201).
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "hash.cuh"
 #include "lookup.cuh"
 #include "reconcile.cuh"
-#include "select_dev.cuh"
 #include "select_fused.cuh"
 
 namespace clo {
 
 namespace {
 
-constexpr int kThreads = kScoreThreads;  // 256
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPieceRows = 1024;
-constexpr int kPieces = kScoreChunk / kPieceRows;
+constexpr int kStages = 3;  // score ring depth (pieces of kPieceRows code rows in flight)
+constexpr int kMaxBins = 8 * 64 + 1;  // nb = bits + 1 <= 513
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t remote(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bulk::smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ int ld_remote_i32(const void* p, uint32_t rank) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(remote(p, rank)) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_remote_u64(const void* p, uint32_t rank) {
+    uint64_t v;
+    asm volatile("ld.shared::cluster.b64 %0, [%1];" : "=l"(v) : "r"(remote(p, rank)) : "memory");
     return v;
 }
 
-// thread 0 waits until *p >= target; the barrier then orders every thread's
-// later reads after the producers' releases (fence + atomic)
-__device__ __forceinline__ void wait_at_least(const int* p, int target) {
-    if (threadIdx.x == 0) {
-        int ns = 32;
-        while (ld_acquire(p) < target) {
-            __nanosleep(ns);
-            ns = ns < 512 ? 2 * ns : ns;
-        }
+// Ascending compaction of keys [start, end) (shared memory; row index =
+// row_off + position): keeps S > T and the first `take` ties S == T (index
+// order), writing at out[base...]. Warp w owns
+// a contiguous 1/8 of the rows: pass 1 counts, an 8-warp prefix orders the
+// warps, pass 2 emits with ballot ranks. Whole CTA; returns the rows written
+// and sets *ties to the ties among them (block-uniform).
+__device__ __forceinline__ int compact_rows(const uint16_t* keys, int start, int end, int row_off, uint16_t T, int base,
+                                            int take, int32_t* out, int* s_gt, int* s_eq, int* ties) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int per = ((end - start + kWarps - 1) / kWarps + 31) / 32 * 32;
+    const int w0 = min(end, start + warp * per), w1 = min(end, w0 + per);
+    int gt = 0, eq = 0;
+    for (int r = w0 + lane; r < w1; r += 32) {
+        const uint16_t kv = keys[r];
+        gt += kv > T;
+        eq += kv == T;
+    }
+    gt = __reduce_add_sync(0xffffffffu, gt);
+    eq = __reduce_add_sync(0xffffffffu, eq);
+    if (lane == 0) {
+        s_gt[warp] = gt;
+        s_eq[warp] = eq;
     }
     __syncthreads();
-}
-
-// thread 0: publish this CTA's writes, then count one more done; returns the
-// previous value (broadcast through *s_old)
-__device__ __forceinline__ int signal_done(int* counter, int* s_old) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *s_old = atomicAdd(counter, 1);
-    __syncthreads();
-    return *s_old;
-}
-
-// S(i) of one 4096-row chunk (rows streamed by cp.async.bulk in 1024-row
-// pieces through a 2-stage ring), keys as u16 and the chunk histogram.
-// `uses` counts this CTA's completed uses of each ring barrier (phase bits).
-template <int W>
-__device__ void score_chunk(const SelArgs& a, int item, int chunk, uint64_t* stage, uint32_t* whist, uint64_t* qb,
-                            uint64_t* bar, uint32_t (&uses)[2]) {
-    const SelItem it = a.items[item];
-    const int c0 = chunk * kScoreChunk;
-    const int end = min(c0 + kScoreChunk, it.n);
-    const int npieces = (end - c0 + kPieceRows - 1) / kPieceRows;
-    const int warp = threadIdx.x >> 5;
-    for (int x = threadIdx.x; x < kWarps * a.nb; x += blockDim.x) whist[x] = 0;
-    for (int x = threadIdx.x; x < a.m * W; x += blockDim.x) {
-        const int j = x / W, w = x % W;
-        qb[x] = a.qbits[((size_t)item * a.m + j) * a.words + w];
-    }
-    __syncthreads();  // also: the previous task's reads of the ring are done
-    auto issue = [&](int p) {  // thread 0
-        const int row0 = c0 + p * kPieceRows;
-        const int rows = min(kPieceRows, end - row0);
-        const uint64_t* src = it.codes + (size_t)row0 * W;
-        const uint32_t bytes = (reinterpret_cast<uintptr_t>(src) & 15) ? 0u : (uint32_t)rows * W * 8 / 16 * 16;
-        uint64_t* b = &bar[p & 1];
-        if (bytes) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk::load_async(stage + (size_t)(p & 1) * kPieceRows * W, src, bytes, b);
-        } else {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bulk::smem_u32(b)) : "memory");
+    int eq_before = 0, pos = base, total = 0, tie_total = 0;
+    for (int w = 0; w < kWarps; ++w) {
+        const int tw = max(0, min(s_eq[w], take - tie_total));
+        if (w < warp) {
+            pos += s_gt[w] + tw;
+            eq_before += s_eq[w];
         }
-    };
-    if (threadIdx.x == 0) {
-        issue(0);
-        if (npieces > 1) issue(1);
+        total += s_gt[w] + tw;
+        tie_total += tw;
     }
-    uint16_t* keys = a.key16 + (size_t)item * a.nmax;
-    uint32_t* myhist = whist + warp * a.nb;
-    for (int p = 0; p < npieces; ++p) {
-        const int row0 = c0 + p * kPieceRows;
-        const int rows = min(kPieceRows, end - row0);
-        bulk::wait(&bar[p & 1], uses[p & 1] & 1);
-        const uint64_t* st = stage + (size_t)(p & 1) * kPieceRows * W;
-        const bool staged = (reinterpret_cast<uintptr_t>(it.codes + (size_t)row0 * W) & 15) == 0;
-        const int copied = staged ? rows * W * 8 / 16 * 16 / (W * 8) : 0;
-#pragma unroll 4
-        for (int r = threadIdx.x; r < rows; r += kThreads) {
-            uint64_t c[W];
-            if (r < copied) {
-#pragma unroll
-                for (int w = 0; w < W; ++w) c[w] = st[(size_t)r * W + w];
-            } else {
-#pragma unroll
-                for (int w = 0; w < W; ++w) c[w] = __ldg(it.codes + (size_t)(row0 + r) * W + w);
-            }
-            int best = 0;
-            for (int j = 0; j < a.m; ++j) {
-                int dist = 0;
-#pragma unroll
-                for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qb[j * W + w]);
-                best = max(best, a.bits - dist);
-            }
-            keys[row0 + r] = static_cast<uint16_t>(best);
-            atomicAdd(&myhist[best], 1u);
-        }
-        ++uses[p & 1];
-        __syncthreads();  // ring slot p & 1 is free again
-        if (threadIdx.x == 0 && p + 2 < npieces) issue(p + 2);
+    for (int r0 = w0; r0 < w1; r0 += 32) {
+        const int r = r0 + lane;
+        const bool valid = r < w1;
+        const uint16_t kv = valid ? keys[r] : (uint16_t)0;
+        const bool is_eq = valid && kv == T;
+        const unsigned eqm = __ballot_sync(0xffffffffu, is_eq);
+        const bool sel = (valid && kv > T) || (is_eq && eq_before + __popc(eqm & lt) < take);
+        const unsigned selm = __ballot_sync(0xffffffffu, sel);
+        if (sel) out[pos + __popc(selm & lt)] = row_off + r;
+        pos += __popc(selm);
+        eq_before += __popc(eqm);
     }
-    uint32_t* out = a.chunk_hist + ((size_t)item * a.max_chunks + chunk) * a.nb;
-    for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
-        uint32_t sum = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) sum += whist[w * a.nb + b];
-        out[b] = sum;
-    }
+    __syncthreads();  // s_gt / s_eq reusable
+    *ties = tie_total;
+    return total;
 }
 
-template <int W>
-__global__ void __launch_bounds__(kThreads) layer_select_kernel(FusedSelectArgs f) {
+template <int W, int CS>
+__global__ void __launch_bounds__(kThreads) layer_select_cluster_kernel(FusedSelectArgs f) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[3];  // score ring (2), P slice (1)
+    __shared__ __align__(8) uint64_t bar[kStages + 1];  // score ring, P slice
     __shared__ LookupShared lsh;
     __shared__ ReconcileSmem<kThreads> rsm;
-    __shared__ int s_task, s_old, s_sts[2], s_gt[kWarps], s_eq[kWarps];
+    __shared__ uint64_t s_qw[kMaxGroup * W];  // the words this rank hashed [j][w]
+    __shared__ uint64_t s_qb[kMaxGroup * W];  // every word of the m queries
+    __shared__ uint32_t s_hist[kMaxBins];     // this rank's histogram of S
+    __shared__ uint32_t s_tot[kMaxBins];      // the item's histogram
+    __shared__ int s_cnt[2], s_T[2], s_gt[kWarps], s_eq[kWarps];
     const PrepareArgs& pa = f.prep;
-    const SelArgs& sa = f.sel;
     const EngineView& v = pa.v;
-    const int l = pa.layer;
-    const int BH = v.B * v.H, NC = sa.max_chunks;
-    int* ctl = f.ctl + (size_t)l * f.ctl_stride;
-    int* claim = ctl;
-    int* lookups_done = ctl + 1;
-    int* score_done = ctl + 2;                   // [items_cap]
-    int* thr_ready = score_done + f.items_cap;   // [items_cap]
-    int* compact_done = thr_ready + f.items_cap; // [items_cap]
-    uint32_t uses[2] = {0, 0};
-    uint32_t slice_uses = 0;
+    const int l = pa.layer, m = v.m, nb = v.bits + 1;
+    const uint32_t rank = cluster_rank();
+    unsigned long long tp[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    CLO_PROBE_T(tp, 0)
+    const int bg = blockIdx.x / CS;
+    const int b = bg / v.H, g = bg % v.H, lg = l * v.H + g;
+    if (v.persistent[lg]) return;  // uniform over the cluster
+    const int seg = (b * v.L + l) * v.H + g;
+    const int t = *v.dev_step + 1;
+    const int n = v.n_prompt + t - 1;  // pre-append pool (engine.cpp:253-255)
+
+    // shared memory: [keys of this rank's rows, u16][work area]; the work area
+    // holds the P slice + queries + labels (lookup, hash), then the score ring
+    // + per-warp histograms, then reconcile's lists
+    const int per = ((n + CS - 1) / CS + kPieceRows - 1) / kPieceRows * kPieceRows;
+    uint16_t* skeys = reinterpret_cast<uint16_t*>(smem);
+    unsigned char* work = smem + f.keys_bytes;
+    double* ps = reinterpret_cast<double*>(work);  // P slice [d][64]
+    double* q = ps + (size_t)v.d * 64;             // [m][d]
+    double* lab_s = q + (size_t)m * v.d;           // [m][d]
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 3; ++i) bulk::mbar_init(&bar[i]);
+        lsh.selected = 0;
+        for (int i = 0; i < kStages + 1; ++i) bulk::mbar_init(&bar[i]);
+    }
+    lookup_stage(pa, b, g, rank == 0, q, lab_s);
+    if (rank == 0) lookup_decide(pa, b, g, q, lab_s, lsh);
+    cluster_sync();
+    const int selected = rank == 0 ? lsh.selected : ld_remote_i32(&lsh.selected, 0);
+    const int item = rank == 0 ? lsh.item : ld_remote_i32(&lsh.item, 0);
+    CLO_PROBE_T(tp, 1)
+    cluster_sync();  // rank 0's decision has been read
+    if (!selected) return;
+
+    // ---- query sign bits: rank r hashes words r, r + CS, ...
+    uint32_t slice_uses = 0;
+    const double* pbase = v.proj_w + (size_t)lg * W * v.d * 64;
+    for (int w = rank; w < W; w += CS) {
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk::load_async(ps, pbase + (size_t)w * v.d * 64, (uint32_t)v.d * 64 * 8, &bar[kStages]);
+        }
+        bulk::wait(&bar[kStages], slice_uses & 1);
+        ++slice_uses;
+        hash_word(ps, q, v.d, m, v.d, w, v.bits, [&](int j) { return reinterpret_cast<uint32_t*>(s_qw + j * W); });
+        __syncthreads();
+    }
+    CLO_PROBE_T(tp, 2)
+    cluster_sync();
+    for (int x = threadIdx.x; x < m * W; x += blockDim.x) s_qb[x] = ld_remote_u64(&s_qw[x], (uint32_t)((x % W) % CS));
+    for (int x = threadIdx.x; x < nb; x += blockDim.x) s_hist[x] = 0;
+
+    // ---- score rows [r0, r1): S(i) = max_j (bits - popcount(q_j ^ code_i))
+    const int r0 = min(n, (int)rank * per), r1 = min(n, r0 + per);
+    const uint64_t* codes = v.codes + (size_t)seg * v.code_stride;
+    {
+        uint64_t* stage = reinterpret_cast<uint64_t*>(work);                                   // [kStages][kPieceRows * W]
+        uint32_t* whist = reinterpret_cast<uint32_t*>(work + kStages * kPieceRows * W * 8);  // [kWarps][nb]
+        for (int x = threadIdx.x; x < kWarps * nb; x += blockDim.x) whist[x] = 0;
+        const int npieces = (r1 - r0 + kPieceRows - 1) / kPieceRows;
+        auto issue = [&](int p) {  // thread 0
+            const int row0 = r0 + p * kPieceRows;
+            const int rows = min(kPieceRows, r1 - row0);
+            const uint64_t* src = codes + (size_t)row0 * W;
+            const uint32_t bytes = (reinterpret_cast<uintptr_t>(src) & 15) ? 0u : (uint32_t)rows * W * 8 / 16 * 16;
+            if (bytes) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bulk::load_async(stage + (size_t)(p % kStages) * kPieceRows * W, src, bytes, &bar[p % kStages]);
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bulk::smem_u32(&bar[p % kStages])) : "memory");
+            }
+        };
+        __syncthreads();  // whist cleared; every thread is done with the P slice
+        if (threadIdx.x == 0)
+            for (int p = 0; p < kStages && p < npieces; ++p) issue(p);
+        uint32_t* myhist = whist + (threadIdx.x >> 5) * nb;
+        for (int p = 0; p < npieces; ++p) {
+            const int row0 = r0 + p * kPieceRows;
+            const int rows = min(kPieceRows, r1 - row0);
+            bulk::wait(&bar[p % kStages], (p / kStages) & 1);
+            const uint64_t* st = stage + (size_t)(p % kStages) * kPieceRows * W;
+            const bool staged = (reinterpret_cast<uintptr_t>(codes + (size_t)row0 * W) & 15) == 0;
+            const int copied = staged ? rows * W * 8 / 16 * 16 / (W * 8) : 0;
+#pragma unroll 4
+            for (int r = threadIdx.x; r < rows; r += kThreads) {
+                uint64_t c[W];
+                if (r < copied) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) c[w] = st[(size_t)r * W + w];
+                } else {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) c[w] = __ldg(codes + (size_t)(row0 + r) * W + w);
+                }
+                int best = 0;
+                for (int j = 0; j < m; ++j) {
+                    int dist = 0;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ s_qb[j * W + w]);
+                    best = max(best, v.bits - dist);
+                }
+                skeys[row0 - r0 + r] = static_cast<uint16_t>(best);
+                atomicAdd(&myhist[best], 1u);
+            }
+            __syncthreads();  // ring slot p % kStages is free again
+            if (threadIdx.x == 0 && p + kStages < npieces) issue(p + kStages);
+        }
+        for (int x = threadIdx.x; x < nb; x += blockDim.x) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s += whist[w * nb + x];
+            s_hist[x] = s;
+        }
+    }
+    CLO_PROBE_T(tp, 3)
+    cluster_sync();
+
+    // ---- threshold (every rank, from the CS histograms): T = k-th largest S,
+    //      ties S == T to keep = k - #(S > T)
+    for (int x = threadIdx.x; x < nb; x += blockDim.x) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int r = 0; r < CS; ++r) s += (uint32_t)ld_remote_i32(&s_hist[x], (uint32_t)r);
+        s_tot[x] = s;
     }
     __syncthreads();
-    for (;;) {
-        if (threadIdx.x == 0) s_task = atomicAdd(claim, 1);
-        __syncthreads();
-        const int t = s_task;
-        if (t < BH) {
-            // ---- lookup (+ query hash on a miss)
-            const int b = t / v.H, g = t % v.H;
-            double* ps = reinterpret_cast<double*>(smem);   // P slice [d][64]
-            double* q = ps + (size_t)v.d * 64;              // [m][d]
-            double* lab_s = q + (size_t)v.m * v.d;          // [m][d]
-            if (v.persistent[l * v.H + g] == 0) {
-                lookup_stage(pa, b, g, true, q, lab_s);
-                lookup_decide(pa, b, g, q, lab_s, lsh);
-                if (lsh.selected) {
-                    const int item = lsh.item;
-                    const double* base = v.proj_w + (size_t)(l * v.H + g) * v.words * v.d * 64;
-                    uint32_t* out32 = reinterpret_cast<uint32_t*>(pa.s.qbits + (size_t)item * v.m * v.words);
-                    for (int w = 0; w < v.words; ++w) {
-                        if (threadIdx.x == 0) {
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            bulk::load_async(ps, base + (size_t)w * v.d * 64, (uint32_t)v.d * 64 * 8, &bar[2]);
-                        }
-                        bulk::wait(&bar[2], slice_uses & 1);
-                        ++slice_uses;
-                        hash_word(ps, q, v.d, v.m, v.d, w, v.bits,
-                                  [&](int j) { return out32 + (size_t)j * v.words * 2; });
-                        __syncthreads();  // the slice buffer is free
-                    }
-                }
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int running = 0, T = -1, gtT = 0;
+        for (int top = nb - 1; top >= 0 && T < 0; top -= 32) {
+            const int bi = top - lane;
+            const int val = bi >= 0 ? (int)s_tot[bi] : 0;
+            int incl = val;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
-            signal_done(lookups_done, &s_old);
-            continue;
-        }
-        wait_at_least(lookups_done, BH);
-        const int C = *reinterpret_cast<const volatile int*>(sa.count);
-        int u = t - BH;
-        if (u < C * NC) {
-            // ---- score one chunk; the item's last chunk computes its threshold
-            const int item = u / NC, chunk = u % NC;
-            const int nch = num_chunks(sa.items[item].n);
-            if (chunk >= nch) continue;
-            uint64_t* stage = reinterpret_cast<uint64_t*>(smem);
-            uint32_t* whist = reinterpret_cast<uint32_t*>(smem + 2 * kPieceRows * W * 8);
-            uint64_t* qb = reinterpret_cast<uint64_t*>(smem + 2 * kPieceRows * W * 8 +
-                                                       ((size_t)kWarps * sa.nb * 4 + 7) / 8 * 8);
-            score_chunk<W>(sa, item, chunk, stage, whist, qb, bar, uses);
-            if (signal_done(score_done + item, &s_old) == nch - 1) {
-                __threadfence();
-                threshold_item(sa, item, reinterpret_cast<uint32_t*>(smem), s_sts);
-                signal_done(thr_ready + item, &s_old);
+            const unsigned hit = __ballot_sync(0xffffffffu, bi >= 0 && running + incl >= v.k);
+            if (hit) {
+                const int first = __ffs(hit) - 1;
+                gtT = running + __shfl_sync(0xffffffffu, incl - val, first);
+                T = top - first;
             }
-            continue;
+            running += __shfl_sync(0xffffffffu, incl, 31);
         }
-        u -= C * NC;
-        if (u < C * NC) {
-            // ---- compact one chunk; the item's last chunk reconciles the entry
-            const int item = u / NC, chunk = u % NC;
-            const int nch = num_chunks(sa.items[item].n);
-            if (chunk >= nch) continue;
-            wait_at_least(thr_ready + item, 1);
-            compact_unit<uint16_t>(sa, item, chunk, s_gt, s_eq);
-            if (signal_done(compact_done + item, &s_old) == nch - 1) {
-                __threadfence();
-                reconcile_item<kThreads>(f.rec, item, reinterpret_cast<int32_t*>(smem), rsm);
-            }
-            continue;
+        if (lane == 0) {
+            s_T[0] = T;
+            s_T[1] = v.k - gtT;  // ties to keep
         }
-        break;
     }
+    __syncthreads();
+    CLO_PROBE_T(tp, 4)
+    const uint16_t T = (uint16_t)s_T[0];
+    const int need_eq = s_T[1];
+    {  // this rank's rows > T and == T
+        int gt = 0, eq = 0;
+        for (int r = threadIdx.x; r < r1 - r0; r += blockDim.x) {
+            const uint16_t kv = skeys[r];
+            gt += kv > T;
+            eq += kv == T;
+        }
+        gt = __reduce_add_sync(0xffffffffu, gt);
+        eq = __reduce_add_sync(0xffffffffu, eq);
+        if ((threadIdx.x & 31) == 0) {
+            s_gt[threadIdx.x >> 5] = gt;
+            s_eq[threadIdx.x >> 5] = eq;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int G = 0, E = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                G += s_gt[w];
+                E += s_eq[w];
+            }
+            s_cnt[0] = G;
+            s_cnt[1] = E;
+        }
+    }
+    CLO_PROBE_T(tp, 5)
+    cluster_sync();
+    // output offset and tie quota of this rank (ties go by ascending index = rank order)
+    int base = 0, quota = 0;
+    {
+        int eq_before = 0;
+        for (int r = 0; r < CS; ++r) {
+            const int gr = ld_remote_i32(&s_cnt[0], (uint32_t)r), er = ld_remote_i32(&s_cnt[1], (uint32_t)r);
+            const int take = max(0, min(er, need_eq - eq_before));
+            if (r < (int)rank) base += gr + take;
+            if (r == (int)rank) quota = take;
+            eq_before += er;
+        }
+    }
+    __syncthreads();  // s_gt / s_eq were read above
+    int32_t* out = f.prep.s.sel + (size_t)item * v.k;  // offloaded heads select into scratch (delta reconcile)
+    for (int c0 = 0; c0 < r1 - r0; c0 += kScoreChunk) {
+        int ties = 0;
+        base += compact_rows(skeys, c0, min(r1 - r0, c0 + kScoreChunk), r0, T, base, quota, out, s_gt, s_eq, &ties);
+        quota -= ties;
+    }
+    CLO_PROBE_T(tp, 6)
+    cluster_sync();  // the whole selection is written; no rank's shared memory is read after this
+    if (rank != 0) return;
+    reconcile_item<kThreads>(f.rec, item, reinterpret_cast<int32_t*>(work), rsm);
+#ifdef CLO_PROBE
+    CLO_PROBE_T(tp, 7)
+    if (threadIdx.x == 0 && l == 6 && t == 12)
+        printf("SEL %llu b%d g%d: lookup %llu hash %llu score %llu thr %llu count %llu compact %llu reconcile %llu\n",
+               tp[0], b, g, tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5],
+               tp[7] - tp[6]);
+#endif
 }
 
 }  // namespace
 
-size_t fused_select_smem(int words, int nb, int m, int d, int k, int max_chunks) {
-    const size_t lookup = (size_t)d * 64 * 8 + 2 * (size_t)m * d * 8;
-    const size_t score = 2 * (size_t)kPieceRows * words * 8 + ((size_t)kWarps * nb * 4 + 7) / 8 * 8 + (size_t)m * words * 8;
-    const size_t thr = ((size_t)nb + 2 * (size_t)max_chunks) * 4;
-    const size_t rec = 4 * (size_t)k * 4;
-    return std::max(std::max(lookup, score), std::max(thr, rec));
+size_t fused_keys_bytes(int nmax, int cs) {
+    const size_t per = ((size_t)(nmax + cs - 1) / cs + kPieceRows - 1) / kPieceRows * kPieceRows;
+    return (per * 2 + 127) / 128 * 128;
 }
 
-void launch_fused_select(const FusedSelectArgs& f, int grid, cudaStream_t stream) {
-    const SelArgs& a = f.sel;
-    const size_t sm = fused_select_smem(a.words, a.nb, a.m, a.d, a.k, a.max_chunks);
-    switch (a.words) {
-#define CLO_W(W)                                                                                           \
-    case W:                                                                                                \
-        cudaFuncSetAttribute(layer_select_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-        layer_select_kernel<W><<<grid, kThreads, sm, stream>>>(f);                                         \
+size_t fused_select_smem(int words, int nb, int m, int d, int k, int nmax, int cs) {
+    const size_t lookup = (size_t)d * 64 * 8 + 2 * (size_t)m * d * 8;
+    const size_t score = (size_t)kStages * kPieceRows * words * 8 + (size_t)kWarps * nb * 4;
+    const size_t rec = 4 * (size_t)k * 4;
+    return fused_keys_bytes(nmax, cs) + std::max(std::max(lookup, score), rec);
+}
+
+bool fused_select_fits(int words, int nb, int m, int d, int k, int nmax) {
+    return fused_select_smem(words, nb, m, d, k, nmax, fused_cluster_size()) <= 200 * 1024;
+}
+
+int fused_cluster_size() {
+    static const int cs = [] {  // CLO_SELECT_CLUSTER: CTAs per missed head (4 or 8)
+        const char* e = getenv("CLO_SELECT_CLUSTER");
+        return e && atoi(e) == 4 ? 4 : 8;
+    }();
+    return cs;
+}
+
+void launch_fused_select(const FusedSelectArgs& f, cudaStream_t stream) {
+    const EngineView& v = f.prep.v;
+    const int cs = fused_cluster_size();
+    const size_t sm = fused_select_smem(v.words, v.bits + 1, v.m, v.d, v.k, v.nmax, cs);
+    FusedSelectArgs fa = f;
+    fa.keys_bytes = (int)fused_keys_bytes(v.nmax, cs);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(v.B * v.H * cs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    switch (v.words * 16 + cs) {
+#define CLO_WC(W, C)                                                                                        \
+    case W * 16 + C:                                                                                        \
+        cudaFuncSetAttribute(layer_select_cluster_kernel<W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)sm);                                                                      \
+        cudaLaunchKernelEx(&cfg, layer_select_cluster_kernel<W, C>, fa);                                     \
         break;
-        CLO_W(1) CLO_W(2) CLO_W(3) CLO_W(4) CLO_W(5) CLO_W(6) CLO_W(7) CLO_W(8)
-#undef CLO_W
+        CLO_WC(1, 4) CLO_WC(2, 4) CLO_WC(3, 4) CLO_WC(4, 4) CLO_WC(5, 4) CLO_WC(6, 4) CLO_WC(7, 4) CLO_WC(8, 4)
+        CLO_WC(1, 8) CLO_WC(2, 8) CLO_WC(3, 8) CLO_WC(4, 8) CLO_WC(5, 8) CLO_WC(6, 8) CLO_WC(7, 8) CLO_WC(8, 8)
+#undef CLO_WC
         default:
             break;
     }

@@ -1,5 +1,6 @@
 // select_fused.cuh — one kernel for a decode layer's whole selection chain
-// (offloaded heads, sign-hash retriever): see select_fused.cu.
+// (offloaded heads, sign-hash retriever), one cluster per (sequence, KV head):
+// see select_fused.cu.
 #pragma once
 
 #include "gather.cuh"
@@ -10,15 +11,15 @@ namespace clo {
 
 struct FusedSelectArgs {
     PrepareArgs prep;   // decode lookup of the layer's offloaded heads (s.items offset to the layer)
-    SelArgs sel;        // the same layer's work list and selection scratch
+    SelArgs sel;        // the layer's selection scratch (u16 keys)
     ReconcileArgs rec;  // its entry reconcile / fetch lists
-    int* ctl;           // [L][ctl_stride] task counters, zeroed at step end
-    int ctl_stride;     // 2 + 3 * items_cap
-    int items_cap;      // B*H
+    int keys_bytes;     // shared memory for one rank's u16 keys (set by the launcher)
 };
 
-inline int fused_ctl_stride(int items_cap) { return 2 + 3 * items_cap; }
-size_t fused_select_smem(int words, int nb, int m, int d, int k, int max_chunks);
-void launch_fused_select(const FusedSelectArgs& f, int grid, cudaStream_t stream);
+size_t fused_select_smem(int words, int nb, int m, int d, int k, int nmax, int cs);
+// the fused kernel holds a rank's keys in shared memory: contexts up to ~512K rows
+bool fused_select_fits(int words, int nb, int m, int d, int k, int nmax);
+int fused_cluster_size();
+void launch_fused_select(const FusedSelectArgs& f, cudaStream_t stream);
 
 }  // namespace clo
