@@ -594,11 +594,11 @@ void Engine::drop_graphs() {  // views and pointers are baked into the graphs
 }
 
 bool Engine::chained_select() const {
-    static const bool off = [] {  // CLO_CHAIN_SELECT=0: separate threshold and reconcile launches
+    static const bool on = [] {  // CLO_CHAIN_SELECT=1: threshold / reconcile by the last CTA per item (slower)
         const char* e = getenv("CLO_CHAIN_SELECT");
-        return e && e[0] == '0';
+        return e && e[0] == '1';
     }();
-    return !off && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && (size_t)cfg_.k * 16 <= 200 * 1024;
+    return on && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && (size_t)cfg_.k * 16 <= 200 * 1024;
 }
 
 ReconcileArgs Engine::reconcile_args(int layer, int fresh) const {

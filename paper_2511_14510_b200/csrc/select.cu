@@ -94,7 +94,61 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Row r's code words from the staged piece: 16-byte loads, the two halves of
+// a row visited in rotated order ((r / (128 / row bytes)) mod chunks) so the
+// eight threads of each shared-memory phase hit eight different 16-byte bank
+// groups (plain row order collides 2-way at 32-byte rows).
 template <int W>
+__device__ __forceinline__ void load_code_row(const uint64_t* st, int r, uint64_t (&c)[W]) {
+    if constexpr (W % 2 == 0 && W * 8 <= 128) {
+        constexpr int kChunks = W / 2;
+        constexpr int kPerGroup = 128 / (W * 8);
+        const int rot = (r / kPerGroup) % kChunks;
+        const ulonglong2* row = reinterpret_cast<const ulonglong2*>(st + (size_t)r * W);
+        ulonglong2 v[kChunks];
+#pragma unroll
+        for (int i = 0; i < kChunks; ++i) v[i] = row[(i + rot) % kChunks];  // v[i] = chunk (i + rot)
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch) {  // register selects, no local-memory indexing
+            ulonglong2 x = v[0];
+#pragma unroll
+            for (int i = 1; i < kChunks; ++i)
+                if ((i + rot) % kChunks == ch) x = v[i];
+            c[2 * ch] = x.x;
+            c[2 * ch + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) c[w] = st[(size_t)r * W + w];
+    }
+}
+
+// S = max_j (bits - popcount(q_j ^ c)); M > 0: group size known at compile
+// time (query words in registers), M == 0: runtime a.m, words from shared memory.
+template <int W, int M>
+__device__ __forceinline__ int score_row(const uint64_t (&c)[W], const uint64_t* qb, const uint64_t (&qr)[M > 0 ? M : 1][W],
+                                         int m, int bits) {
+    int best = 0;
+    if constexpr (M > 0) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            int dist = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qr[j][w]);
+            best = max(best, bits - dist);
+        }
+    } else {
+        for (int j = 0; j < m; ++j) {
+            int dist = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qb[j * W + w]);
+            best = max(best, bits - dist);
+        }
+    }
+    return best;
+}
+
+template <int W, int M>
 __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelArgs a, int agg) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* stage = reinterpret_cast<uint64_t*>(sm);                              // [2][kPieceRows*W]
@@ -169,23 +223,23 @@ __global__ void __launch_bounds__(kScoreThreads) score_signhash_tma_kernel(SelAr
         const int copied = staged ? rows * W * 8 / 16 * 16 / (W * 8) : 0;  // whole rows in smem
         uint16_t* keys = a.key16 + (size_t)item * a.nmax;
         uint32_t* myhist = whist + warp * a.nb;
+        uint64_t qr[M > 0 ? M : 1][W];
+        if constexpr (M > 0) {
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+#pragma unroll
+                for (int w = 0; w < W; ++w) qr[j][w] = qb[j * W + w];
+        }
 #pragma unroll 4
         for (int r = threadIdx.x; r < rows; r += kScoreThreads) {
             uint64_t c[W];
             if (r < copied) {
-#pragma unroll
-                for (int w = 0; w < W; ++w) c[w] = st[(size_t)r * W + w];
+                load_code_row<W>(st, r, c);
             } else {
 #pragma unroll
                 for (int w = 0; w < W; ++w) c[w] = __ldg(codes + (size_t)(row0 + r) * W + w);
             }
-            int best = 0;
-            for (int j = 0; j < a.m; ++j) {
-                int dist = 0;
-#pragma unroll
-                for (int w = 0; w < W; ++w) dist += __popcll(c[w] ^ qb[j * W + w]);
-                best = max(best, a.bits - dist);
-            }
+            const int best = score_row<W, M>(c, qb, qr, a.m, a.bits);
             keys[row0 + r] = static_cast<uint16_t>(best);
             if (agg) {  // warp-aggregated: one shared atomic per distinct score
                 const unsigned act = __activemask();
@@ -453,6 +507,25 @@ __global__ void chunk_prefix_kernel(SelArgs a) {
 
 }  // namespace
 
+// Group sizes with a compile-time kernel (query words in registers); others
+// use the runtime-m kernel.
+template <int W>
+void launch_score_tma(const SelArgs& a, int grid, size_t sm, int agg, cudaStream_t stream) {
+    switch (a.m) {
+#define CLO_M(MM)                                                                                          \
+    case MM:                                                                                               \
+        cudaFuncSetAttribute(score_signhash_tma_kernel<W, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)sm);                                                                     \
+        score_signhash_tma_kernel<W, MM><<<grid, kScoreThreads, sm, stream>>>(a, agg);                     \
+        return;
+        CLO_M(1) CLO_M(2) CLO_M(4) CLO_M(5) CLO_M(8)
+#undef CLO_M
+        default:
+            cudaFuncSetAttribute(score_signhash_tma_kernel<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            score_signhash_tma_kernel<W, 0><<<grid, kScoreThreads, sm, stream>>>(a, agg);
+    }
+}
+
 void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec) {
     const size_t sm_score = (size_t)kWarps * a.nb * 4 + 8 + (size_t)a.m * a.words * 8;
     static const bool tma = [] {  // CLO_SCORE=lsu: the register-load kernel
@@ -474,9 +547,7 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const Reconci
 #define CLO_W(W)                                                                                            \
     case W:                                                                                                 \
         if (tma) {                                                                                          \
-            cudaFuncSetAttribute(score_signhash_tma_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                 (int)sm_tma);                                                              \
-            score_signhash_tma_kernel<W><<<grid_tma, kScoreThreads, sm_tma, stream>>>(a, hist_agg);           \
+            launch_score_tma<W>(a, grid_tma, sm_tma, hist_agg, stream);                                     \
         } else {                                                                                            \
             score_signhash_kernel<W><<<a.grid, kScoreThreads, sm_score, stream>>>(a);                       \
         }                                                                                                   \
