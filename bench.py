@@ -83,6 +83,9 @@ def parse():
                     help="storage type of the K/V rows (host store, cache slots, attention operands)")
     ap.add_argument("--victim-rows", type=int, default=-1,
                     help="HBM rows kept per offloaded head beyond its entry (-1: engine default 8k, 0: none)")
+    ap.add_argument("--no-alias", action="store_true",
+                    help="one host K/V region per layer (no layer aliasing): quantifies the aliased store's "
+                         "effect on the gather; needs L times the host RAM (use --layers/--batch to fit)")
     ap.add_argument("--huge", action="store_true",
                     help="back the pinned host KV store with 2 MiB pages (GPU TLB reach for large stores)")
     ap.add_argument("--same-device", action="store_true",
@@ -207,7 +210,9 @@ def workload_config(args, plan_info, world):
             "parallelism": (f"kv-head-sharded x{world} (+{'fused P2P' if args.allgather == 'fused' else 'NCCL'} "
                             f"head-output all-gather)" if shard_heads else f"request-sharded x{world}"),
             "l2": "per-step working set (codes, slots, persistent KV) >> 126 MB L2",
-            "host_kv": "pinned, one buffer per (seq, kv head) aliased across layers, "
+            "host_kv": ("pinned, one buffer per (seq, layer, kv head), not aliased, "
+                        if getattr(args, "no_alias", False) else
+                        "pinned, one buffer per (seq, kv head) aliased across layers, ")
                        + ("K|V rows of a token contiguous (row stride 2d)" if args.kv_layout == "interleaved"
                           else "separate K and V matrices"),
             "kv_dtype": args.kv_dtype, "sigma_step": args.sigma, "sigma_layer": args.sigma_layer,
@@ -395,16 +400,18 @@ def run_ours(args):
     kvd = args.kv_dtype
     tdt = torch.bfloat16 if kvd == "bf16" else torch.float32
     esz = 2 if kvd == "bf16" else 4
-    hkv = HostKV(B, 1, H, nmax, d, kvd, hugepages=args.huge, interleaved=args.kv_layout == "interleaved",
+    Lk = L if args.no_alias else 1
+    hkv = HostKV(B, Lk, H, nmax, d, kvd, hugepages=args.huge, interleaved=args.kv_layout == "interleaved",
                  numa_node=node if numa["bound"] else -1)
     for b in range(B):
-        for arr in (hkv.k, hkv.v):
-            x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
-            for h in range(H):  # contiguous [n][d] block of pinned memory: direct D2H
-                if kvd == "bf16":
-                    torch.from_numpy(arr[b, 0, h, :n].view(np.int16)).copy_(x[h].view(torch.int16))
-                else:
-                    torch.from_numpy(arr[b, 0, h, :n]).copy_(x[h])
+        for lk in range(Lk):
+            for arr in (hkv.k, hkv.v):
+                x = torch.randn((H, n, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+                for h in range(H):  # contiguous [n][d] block of pinned memory: direct D2H
+                    if kvd == "bf16":
+                        torch.from_numpy(arr[b, lk, h, :n].view(np.int16)).copy_(x[h].view(torch.int16))
+                    else:
+                        torch.from_numpy(arr[b, lk, h, :n]).copy_(x[h])
 
     # per-step inputs (device resident): drift-walk queries, layer-invariant new rows
     def norm(x):
@@ -417,8 +424,8 @@ def run_ours(args):
             q = norm(q + args.sigma * torch.randn(q.shape, generator=gen, device=dev))
         tq[t] = q
         aq[t] = norm(q + args.sigma_layer * torch.randn(q.shape, generator=gen, device=dev))
-    nk = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
-    nv = torch.randn((S, B, 1, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
+    nk = torch.randn((S, B, Lk, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
+    nv = torch.randn((S, B, Lk, H, d), generator=gen, device=dev).to(tdt).expand(S, B, L, H, d).contiguous()
     fused_x = shard_heads and args.allgather == "fused"
     HQo = HQ * world if fused_x else HQ  # out's head extent
     out = torch.empty((B, L, HQo, d), device=dev)
@@ -441,7 +448,7 @@ def run_ours(args):
     tau, qimp, persistent = tau[:, sl].copy(), qimp[:, sl].copy(), persistent[:, sl].copy()
 
     class _Src:  # StepSource shape for DecodeEngine's constructor (prompt already in hkv)
-        n_prompt, steps, alias_layers = n, S, True
+        n_prompt, steps, alias_layers = n, S, not args.no_alias
         prompt_k = prompt_v = None
 
     cfg = EngineConfig(shape=ModelShape(L, HQ, H, d, esz), k=k, sink_tokens=4, recent_tokens=64,

@@ -102,7 +102,9 @@ typedef struct clo_engine_config {
     double tau_override;
     int sync_override; /* -1: policy default (engine.cpp:140-142) */
     int collect_outputs;
-    int compute_oracle_error; /* must be 0: the oracle lives in tests */
+    int compute_oracle_error; /* EngineConfig::compute_oracle_error (engine.hpp:48): each step also takes the
+                                 exact top-k with the true queries and accumulates the relative L2 error of
+                                 the outputs against attention over it (a diagnostic: it reads every key) */
     /* --- B200 fields ----------------------------------------------------- */
     int batch;        /* sequences served by this engine (the runner's tasks) */
     int n_prompt;     /* StepSource::prompt_tokens() */
@@ -207,6 +209,8 @@ typedef struct clo_metrics {
     uint64_t host_bytes;             /* host_bytes() per sequence */
     uint64_t device_persistent_bytes;/* device_persistent_bytes() per sequence */
     int sync_mode;                   /* clo_sync_mode */
+    double mean_output_error;        /* DecodeMetrics::mean_output_error over all sequences (0 unless
+                                        compute_oracle_error) */
 } clo_metrics;
 clo_status clo_get_metrics(clo_engine* e, clo_metrics* out);
 

@@ -73,7 +73,7 @@ struct EngineConfig {
     ModeFlags mode;
     std::optional<SyncMode> sync_override;
     bool collect_outputs = false;
-    bool compute_oracle_error = false;
+    bool compute_oracle_error = true;  // engine.hpp:48 (output_error.cu; reads every key each step)
     // B200
     int batch = 1;
     int kv_dtype = CLO_DTYPE_BF16;

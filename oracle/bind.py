@@ -388,6 +388,10 @@ class Reference(_Common):
             _p(outs, C.c_double), buf, C.c_size_t(json_cap)))
         return outs, buf.value.decode()
 
+    def set_compute_oracle_error(self, on: bool) -> None:
+        """EngineConfig::compute_oracle_error (engine.hpp:48) for the following engine runs."""
+        self.lib.ref_set_compute_oracle_error(int(on))
+
     def run_engine(self, cfg: EngineCfg, tau, q_importance, persistent, prompt_k, prompt_v,
                    true_q, approx_q, new_k, new_v, json_cap=1 << 24):
         """Full reference DecodeEngine run; returns (outputs, cache_state_json, step_seconds)."""

@@ -275,6 +275,10 @@ uint64_t ref_cache_bytes(int offloaded, int entry_k, int held, int L, int hq, in
     return cache_bytes(offloaded, entry_k, held, L, hq, d, e);  // similarity_cache.cpp:167-178
 }
 
+static bool g_oracle_error = false;  // EngineConfig::compute_oracle_error for the next runs
+
+void ref_set_compute_oracle_error(int on) { g_oracle_error = on != 0; }
+
 static EngineConfig engine_config_of(const ref_engine_cfg* c) {
     EngineConfig cfg;
     cfg.shape = ModelShape{c->num_layers, c->num_q_heads, c->num_kv_heads, c->head_dim,
@@ -290,7 +294,7 @@ static EngineConfig engine_config_of(const ref_engine_cfg* c) {
     cfg.mode.always_hit = c->always_hit;
     if (c->has_tau_override) cfg.mode.tau_override = c->tau_override;
     cfg.collect_outputs = true;
-    cfg.compute_oracle_error = false;
+    cfg.compute_oracle_error = g_oracle_error;
     return cfg;
 }
 

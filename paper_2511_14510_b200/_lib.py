@@ -101,6 +101,7 @@ class Metrics(C.Structure):
         ("persistent_bytes", C.c_uint64), ("gathered_bytes_device", C.c_uint64),
         ("cache_bytes_current", C.c_uint64), ("host_bytes", C.c_uint64),
         ("device_persistent_bytes", C.c_uint64), ("sync_mode", C.c_int),
+        ("mean_output_error", C.c_double),
     ]
 
 

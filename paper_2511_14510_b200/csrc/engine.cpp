@@ -23,6 +23,7 @@
 #include "lookup.cuh"
 #include "select.cuh"
 #include "select_fused.cuh"
+#include "output_error.cuh"
 
 namespace clo {
 
@@ -92,8 +93,6 @@ Engine::Engine(const clo_engine_config& cfg, const double* tau, const double* q_
     if (cfg.policy != CLO_POLICY_SIMILARITY && cfg.policy != CLO_POLICY_PREFETCH_ONLY)
         fail(CLO_ERR_CONFIG, "unknown policy");
     if (cfg.always_hit && cfg.always_miss) fail(CLO_ERR_CONFIG, "always_hit and always_miss are mutually exclusive");
-    if (cfg.compute_oracle_error)
-        fail(CLO_ERR_CONFIG, "compute_oracle_error is a CPU-oracle metric; run the oracle in tests instead");
     if (cfg.retriever != CLO_RETRIEVER_EXACT && cfg.retriever != CLO_RETRIEVER_SIGN_HASH)
         fail(CLO_ERR_CONFIG, "unknown retriever");
     if (cfg.retriever == CLO_RETRIEVER_SIGN_HASH && (cfg.hash_bits <= 0 || cfg.hash_bits % 8 != 0))
@@ -263,6 +262,11 @@ void Engine::allocate() {
                             pt[(lg * d + c) * cfg_.hash_bits + w * 64 + i];
         d_proj_w_.alloc(sizeof(double) * pw.size(), false);
         CLO_CUDA(cudaMemcpy(d_proj_w_.p, pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
+    }
+    if (cfg_.compute_oracle_error) {  // scratch of output_error.cu (keys, scores, lists, per-sequence sums)
+        const size_t segs = (size_t)B * H, w = (size_t)cfg_.k + cfg_.sink_tokens + cfg_.recent_tokens;
+        d_oerr_.alloc(sizeof(uint64_t) * segs * nmax_ + (sizeof(double) + 2 * sizeof(int32_t)) * segs * w +
+                      sizeof(double) * B * L * HQ + 64);
     }
     d_labels_.alloc(sizeof(double) * B * L * HQ * d);
     d_label_valid_.alloc(sizeof(int) * B * L * HQ);
@@ -591,6 +595,36 @@ void Engine::drop_graphs() {  // views and pointers are baked into the graphs
         execs_[m] = nullptr;
         graphs_[m] = nullptr;
     }
+}
+
+OutputErrorArgs Engine::output_error_args() const {
+    const size_t segs = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
+    const size_t w = (size_t)cfg_.k + cfg_.sink_tokens + cfg_.recent_tokens;
+    char* p = d_oerr_.as<char>();
+    OutputErrorArgs a{};
+    a.keys = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * segs * nmax_;
+    a.scores = reinterpret_cast<double*>(p);
+    p += sizeof(double) * segs * w;
+    a.sel = reinterpret_cast<int32_t*>(p);
+    p += sizeof(int32_t) * segs * w;
+    a.uni = reinterpret_cast<int32_t*>(p);
+    p += sizeof(int32_t) * segs * w;
+    a.err = reinterpret_cast<double*>(p);
+    return a;
+}
+
+double Engine::mean_output_error(int b) {  // DecodeMetrics::mean_output_error (engine.cpp:67-69)
+    if (!cfg_.compute_oracle_error || steps_ == 0) return 0.0;
+    const clo_model_shape& s = cfg_.shape;
+    const size_t per = (size_t)s.num_layers * s.num_q_heads;
+    std::vector<double> e(per);
+    synchronize();
+    CLO_CUDA(cudaMemcpy(e.data(), output_error_args().err + (size_t)b * per, sizeof(double) * per,
+                        cudaMemcpyDeviceToHost));
+    double sum = 0.0;
+    for (double x : e) sum += x;  // fixed order: layer, query head
+    return sum / (double)(per * steps_);
 }
 
 bool Engine::chained_select() const {
@@ -1047,6 +1081,11 @@ void Engine::capture_graph(int mode) {
         prof_end(s_main_, "exchange_finish", -1);
         launches_ += 2;
     }
+    if (cfg_.compute_oracle_error) {  // engine.cpp:257-267, 394-405: exact-top-k output error
+        const OutputErrorArgs oa = output_error_args();
+        for (int l = 0; l < L; ++l) launch_output_error(view(), l, oa, s_main_);
+        launches_ += L;
+    }
     launch_step_end(view(), scratch_[0].count, scratch_[1].count, s_main_);
     launches_ += 1;
     CLO_CUDA(cudaStreamEndCapture(s_main_, graph_out));
@@ -1345,6 +1384,8 @@ clo_metrics Engine::metrics() {
                     : clo_cache_bytes(no_, cfg_.k, no_ ? held_tokens() : 0, s.num_layers, s.num_q_heads,
                                       s.head_dim, s.bytes_per_element);
     m.sync_mode = sync_mode_;
+    m.mean_output_error = 0.0;
+    for (int b = 0; b < cfg_.batch; ++b) m.mean_output_error += mean_output_error(b) / cfg_.batch;
     return m;
 }
 
@@ -1446,8 +1487,9 @@ std::string Engine::cache_state_json(int b) {
     os << ",\n    \"transferred_bytes\": " << tot.misses * entry_bytes()
        << ",\n    \"persistent_served_bytes\": " << (uint64_t)np_ * steps_ * entry_bytes()
        << ",\n    \"cache_bytes\": " << all.cache_bytes_current << ",\n    \"host_bytes\": " << all.host_bytes
-       << ",\n    \"device_persistent_bytes\": " << all.device_persistent_bytes
-       << ",\n    \"mean_output_error\": 0.0\n  },\n  \"layers\": [";
+       << ",\n    \"device_persistent_bytes\": " << all.device_persistent_bytes << ",\n    \"mean_output_error\": ";
+    json_num(os, mean_output_error(b));  // this sequence's DecodeMetrics::mean_output_error
+    os << "\n  },\n  \"layers\": [";
     std::vector<int32_t> idx(cfg_.k);
     std::vector<double> hist(std::max(cfg_.max_steps, 1));
     for (int l = 0; l < s.num_layers; ++l) {

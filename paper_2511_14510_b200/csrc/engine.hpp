@@ -66,6 +66,8 @@ class Engine {
     void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
     void enqueue_select(int which, int layer, cudaStream_t st, bool with_reconcile = false);
     bool chained_select() const;
+    struct OutputErrorArgs output_error_args() const;
+    double mean_output_error(int b);
     ReconcileArgs reconcile_args(int layer, int fresh) const;
     void enqueue_reconcile(int layer, int fresh, cudaStream_t st);
     void enqueue_gather(int layer, int count_bytes, cudaStream_t st);
@@ -108,6 +110,7 @@ class Engine {
     int n_off_layers_ = 0;
     DevBuf d_in_tq_, d_in_aq_, d_in_nk_, d_in_nv_, d_out_;
     DevBuf d_tmaps_;  // 4 CUtensorMaps over the cache slots (attention TMA boxes)
+    DevBuf d_oerr_;   // compute_oracle_error scratch (output_error.cuh)
     // host-input staging, double-buffered: step t+1's H2D copies run on a copy
     // stream while step t's graph still executes
     std::array<DevBuf, 2> d_in_;

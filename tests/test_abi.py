@@ -170,11 +170,13 @@ def test_cpp_shim_decodes_on_gpu_like_the_python_path(tmp_path):
     m = hq // hkv
     tau = np.array([[0.55 + 0.1 * ((l + g) % 4) for g in range(hkv)] for l in range(L)])
     qimp = np.broadcast_to(1.0 + np.arange(m), (L, hkv, m)).copy()
+    # the shim keeps EngineConfig's defaults (engine.hpp:30-49), compute_oracle_error included
     cfg = EngineConfig(shape=ModelShape(L, hq, hkv, d, 4), k=64, retriever="sign_hash", retriever_seed=5,
-                       policy="similarity", mode=ModeFlags(), batch=1, kv_dtype="f32")
+                       policy="similarity", mode=ModeFlags(), batch=1, kv_dtype="f32", compute_oracle_error=True)
     eng = DecodeEngine(cfg, profiles_from_arrays(tau, qimp), PartitionPlan(layers=[list(range(hkv))] + [[]] * (L - 1)),
                        TraceSource(trace, kv_dtype="f32"))
     eng.run()
     py_state = json.loads(eng.cache_state_json())
     assert shim_state["totals"]["misses"] > 0 and shim_state["totals"]["hits"] > 0
+    assert shim_state["totals"]["mean_output_error"] > 0.0
     assert shim_state == py_state
