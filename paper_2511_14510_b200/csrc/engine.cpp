@@ -563,7 +563,7 @@ SelArgs Engine::sel_args(int which, int layer) const {
     a.radix_hist = sc.radix_hist;
     a.grid = grid_for((int64_t)cfg_.batch * s.num_kv_heads * max_chunks_);
     a.max_items = cfg_.batch * s.num_kv_heads;
-    a.item_done = chained_select() ? sc.item_done : nullptr;
+    a.item_done = chained_select() >= 1 ? sc.item_done : nullptr;
     return a;
 }
 
@@ -627,12 +627,18 @@ double Engine::mean_output_error(int b) {  // DecodeMetrics::mean_output_error (
     return sum / (double)(per * steps_);
 }
 
-bool Engine::chained_select() const {
-    static const bool on = [] {  // CLO_CHAIN_SELECT=1: threshold / reconcile by the last CTA per item (slower)
+int Engine::chained_select() const {
+    // CLO_CHAIN_SELECT=thr: the CTA finishing an item's last score chunk computes
+    // its threshold (no threshold launch); =all: also the CTA finishing its last
+    // compaction chunk reconciles it (no reconcile launch); 0: neither
+    static const int mode = [] {
         const char* e = getenv("CLO_CHAIN_SELECT");
-        return e && e[0] == '1';
+        if (!e) return 0;
+        const std::string m(e);
+        return m == "all" || m == "1" ? 2 : (m == "thr" ? 1 : 0);
     }();
-    return on && cfg_.retriever == CLO_RETRIEVER_SIGN_HASH && (size_t)cfg_.k * 16 <= 200 * 1024;
+    if (cfg_.retriever != CLO_RETRIEVER_SIGN_HASH) return 0;
+    return mode == 2 && (size_t)cfg_.k * 16 > 200 * 1024 ? 1 : mode;
 }
 
 ReconcileArgs Engine::reconcile_args(int layer, int fresh) const {
@@ -660,7 +666,7 @@ void Engine::enqueue_select(int which, int layer, cudaStream_t st, bool with_rec
         // decode, offloaded heads, chained stages: the compaction kernel also
         // reconciles each item's entry (one launch instead of two)
         const ReconcileArgs ra = reconcile_args(layer, 0);
-        launch_select_signhash(a, st, with_reconcile && a.item_done ? &ra : nullptr);
+        launch_select_signhash(a, st, with_reconcile && chained_select() == 2 ? &ra : nullptr);
         launches_ += a.item_done ? 2 : 3;
     } else {
         launch_select_exact(a, st);
@@ -1034,7 +1040,7 @@ void Engine::capture_graph(int mode) {
             } else {
                 enqueue_prepare(1, l, kPrepDecode, kKindOffloaded, s_pref);
                 enqueue_select(1, l, s_pref, true);
-                if (!chained_select()) enqueue_reconcile(l, 0, s_pref);
+                if (chained_select() < 2) enqueue_reconcile(l, 0, s_pref);
             }
             if (!flags) {
                 // one gather launch per layer, ordered by graph edges

@@ -65,7 +65,7 @@ class Engine {
     SelArgs sel_args(int which, int layer) const;
     void enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st);
     void enqueue_select(int which, int layer, cudaStream_t st, bool with_reconcile = false);
-    bool chained_select() const;
+    int chained_select() const;
     struct OutputErrorArgs output_error_args() const;
     double mean_output_error(int b);
     ReconcileArgs reconcile_args(int layer, int fresh) const;
