@@ -321,21 +321,45 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gpm = (v.k + kTmaRows - 1) / kTmaRows;  // 32-row groups per matrix
     const bool fused = v.kv_fused;                    // one [K|V] token run per lane and group
     const int nmat = fused ? 1 : 2;
     const int cbytes = fused ? 2 * row_bytes : row_bytes;  // bytes copied per row
-    const int total = a.count[a.layer] * nmat * gpm;
     const int wpc = blockDim.x >> 5;
     const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
-    const int mine = total > gw ? (total - 1 - gw) / nw + 1 : 0;
     char* st0 = tstage + (size_t)warp * stages * kTmaRows * cbytes;
-    if (lane == 0) {
+    // The layer's NON-EMPTY 32-row groups as one flat list (a move list holds
+    // fetch_count <= k rows): gpref[i] = first flat group of item i. Warps take
+    // flat groups gw, gw + nw, ... so every warp gets the same number of real
+    // groups (+-1) and none walks empty ones.
+    int* gpref = reinterpret_cast<int*>(tstage + (size_t)wpc * stages * kTmaRows * cbytes *
+                                                     (v.pool > v.k ? 2 : 1));
+    const int count = a.count[a.layer];
+    if (warp == 0) {
+        int run = 0;
+        for (int i0 = 0; i0 < count; i0 += 32) {
+            const int i = i0 + lane;
+            const int fc = i < count ? a.fetch_count[(size_t)a.layer * a.items_cap + i] : 0;
+            const int gi = nmat * ((fc + kTmaRows - 1) / kTmaRows);
+            int incl = gi;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (i < count) gpref[i] = run + incl - gi;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) gpref[count] = run;
+        for (int s = 0; s < stages && lane == 0; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[warp][s])));
+    } else if (lane == 0) {
         for (int s = 0; s < stages; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[warp][s])));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
+    if (lane == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const int total = gpref[count];
+    const int mine = total > gw ? (total - 1 - gw) / nw + 1 : 0;
     // Row of group i handled by this lane: destination entry slot in its
     // matrix (K, or K then V for fused runs), source = the host row (`host`
     // set) or the victim slot `prom` of a promotion; `dem` = the victim slot
@@ -348,10 +372,20 @@ __global__ void __launch_bounds__(kTmaWarps * 32) gather_engine_tma_kernel(Gathe
     auto locate = [&](int i) {
         Row r{};
         const int gidx = gw + i * nw;
-        const int item = gidx / (nmat * gpm), rem = gidx % (nmat * gpm), grp = rem % gpm;
-        r.mat = rem / gpm;
+        int lo = 0, hi = count;  // the item whose flat range holds gidx: gpref[item] <= gidx < gpref[item + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (gpref[mid] <= gidx)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const int item = lo;
         const size_t li = (size_t)a.layer * a.items_cap + item;
         const int nf = a.fetch_count[li];
+        const int gi = (nf + kTmaRows - 1) / kTmaRows;  // groups per matrix of this item
+        const int rem = gidx - gpref[item], grp = rem % gi;
+        r.mat = rem / gi;
         r.rows = max(0, min(kTmaRows, nf - grp * kTmaRows));
         r.prom = -1;
         r.dem = -1;
@@ -516,7 +550,8 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     const int row_bytes = v.d * dtype_size(v.kv_dtype);
     const int vpr = row_bytes / 16;
     const int cbytes = v.kv_fused ? 2 * row_bytes : row_bytes;
-    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * cbytes * (v.pool > v.k ? 2 : 1);  // + demotion stage
+    const size_t sm = (size_t)shape.x * shape.y * kTmaRows * cbytes * (v.pool > v.k ? 2 : 1)  // + demotion stage
+                      + ((size_t)a.items_cap + 1) * sizeof(int);                                 // + group prefix
     const bool small_region = (int64_t)v.nmax * row_bytes <= (int64_t)48 << 20;  // between the measured 32 / 64 MiB points
     const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
     if (use == 2 && sm <= 200 * 1024) {
@@ -527,11 +562,13 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
         gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
         return;
     }
-    // PCIe needs well over 100 KB in flight; 48 CTAs x 32 KiB saturate the
-    // link and leave most SMs to the selection and attention kernels.
+    // PCIe needs well over 100 KB in flight; 24 CTAs x 32 KiB keep the link
+    // busy over large host regions with a shallower queue of host reads (every
+    // kernel boundary elsewhere waits for that queue): configs[3] 872 / 969
+    // tokens/s vs 864 / 900 with 48 CTAs on two boxes (profiles/r2).
     const int64_t units = v.kv_fused ? (int64_t)a.items_cap * ((v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs)
                                      : (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 24, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 
