@@ -129,6 +129,217 @@ __device__ __forceinline__ void gather_unit(const GatherEngineArgs& a, int layer
     }
 }
 
+// "Wide" LSU gather: few fat CTAs (T threads x U 16-byte loads in flight each)
+// over a flat list of the layer's moved rows. With a shared-memory
+// reservation that no other kernel's CTA fits beside, the gather owns a few
+// SMs and the host reads queue only there: kernel boundaries elsewhere wait
+// for the SM's own outstanding reads (profiles/r2: 2 us beside a gather on
+// 16 SMs, 37 us beside one spread over 128). CLO_GATHER=wide (experiment).
+template <int T, int U>
+__global__ void __launch_bounds__(T) gather_wide_kernel(GatherEngineArgs a) {
+    extern __shared__ int wpref[];  // [count + 1] first flat row of each item (then the reservation)
+    const EngineView& v = a.v;
+    const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int vpr = row_bytes / 16;
+    const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);
+    const bool fused = v.kv_fused;
+    const int vpt = 2 * vpr;  // K then V vectors of a moved row
+    const int count = a.count[a.layer];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        int run = 0;
+        for (int i0 = 0; i0 < count; i0 += 32) {
+            const int i = i0 + lane;
+            const int fc = i < count ? a.fetch_count[(size_t)a.layer * a.items_cap + i] : 0;
+            int incl = fc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (i < count) wpref[i] = run + incl - fc;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) wpref[count] = run;
+    }
+    __syncthreads();
+    const long long total = (long long)wpref[count] * vpt;
+    const size_t esz = dtype_size(v.kv_dtype);
+    unsigned long long moved = 0;
+    for (long long base = (long long)blockIdx.x * T * U; base < total; base += (long long)gridDim.x * T * U) {
+        uint4 r[U], old[U];
+        uint4* dp[U];
+        uint4* vp[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const long long e = base + (long long)uu * T + threadIdx.x;
+            dp[uu] = nullptr;
+            vp[uu] = nullptr;
+            if (e < total) {
+                const int fr = (int)(e / vpt), c = (int)(e - (long long)fr * vpt);
+                int lo = 0, hi = count;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (wpref[mid] <= fr)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                const size_t li = (size_t)a.layer * a.items_cap + lo;
+                const int j = fr - wpref[lo];
+                const int seg = a.items[li].seg;
+                const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+                const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+                const bool isv = c >= vpr;
+                const int cc = isv ? c - vpr : c;
+                uint4* pool = reinterpret_cast<uint4*>((char*)(isv ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
+                const int slot = a.fetch_slot[li * v.k + j], src = a.fetch_tok[li * v.k + j];
+                const int dem = a.fetch_dem[li * v.k + j];
+                dp[uu] = pool + (size_t)slot * vpr + cc;
+                if (dem >= 0) {
+                    old[uu] = *dp[uu];
+                    vp[uu] = pool + (size_t)dem * vpr + cc;
+                }
+                if (src >= 0) {
+                    const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+                    const uint4* hs = reinterpret_cast<const uint4*>(
+                        (const char*)(fused || !isv ? v.host_k : v.host_v) + hb * esz);
+                    r[uu] = hs[(size_t)src * rvpr + (fused ? c : cc)];
+                    ++moved;
+                } else {
+                    r[uu] = pool[(size_t)(-src - 1) * vpr + cc];
+                }
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            if (vp[uu]) *vp[uu] = old[uu];
+            if (dp[uu]) *dp[uu] = r[uu];
+        }
+    }
+    if (a.count_bytes) {
+        moved = __reduce_add_sync(0xffffffffu, (unsigned)moved);
+        if (lane == 0 && moved) atomicAdd(v.gathered_bytes, moved * 16ull);
+    }
+}
+
+// Wide gather with the rows in flight held in SHARED memory (cp.async 16-byte
+// copies, LDGSTS) instead of registers: T threads x U vectors per batch, two
+// batches in flight per CTA (the next batch's host reads are issued before the
+// current batch is stored), so a few CTAs keep megabytes of host reads in
+// flight on their own SMs. CLO_GATHER=wide_smem (experiment).
+template <int T, int U>
+__global__ void __launch_bounds__(T) gather_wide_smem_kernel(GatherEngineArgs a) {
+    extern __shared__ __align__(16) unsigned char wsm[];  // [2][U][T] uint4, then [count + 1] row prefix
+    uint4* buf = reinterpret_cast<uint4*>(wsm);
+    int* wpref = reinterpret_cast<int*>(wsm + 2 * (size_t)U * T * sizeof(uint4));
+    const EngineView& v = a.v;
+    const int row_bytes = v.d * dtype_size(v.kv_dtype);
+    const int vpr = row_bytes / 16;
+    const int rvpr = (int)(v.row_stride * (int64_t)dtype_size(v.kv_dtype) / 16);
+    const bool fused = v.kv_fused;
+    const int vpt = 2 * vpr;
+    const int count = a.count[a.layer];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        int run = 0;
+        for (int i0 = 0; i0 < count; i0 += 32) {
+            const int i = i0 + lane;
+            const int fc = i < count ? a.fetch_count[(size_t)a.layer * a.items_cap + i] : 0;
+            int incl = fc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (i < count) wpref[i] = run + incl - fc;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) wpref[count] = run;
+    }
+    __syncthreads();
+    const long long total = (long long)wpref[count] * vpt;
+    const size_t esz = dtype_size(v.kv_dtype);
+    // vector e of the flat list: its pool row base (K or V pool of its head)
+    // and slot, plus the source (host row, or victim slot for a promotion)
+    struct Vec {
+        uint4* pool;
+        int slot, dem, cc;
+        const uint4* src;
+    };
+    auto locate = [&](long long e) {
+        Vec x;
+        const int fr = (int)(e / vpt), c = (int)(e - (long long)fr * vpt);
+        int lo = 0, hi = count;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (wpref[mid] <= fr)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const size_t li = (size_t)a.layer * a.items_cap + lo;
+        const int j = fr - wpref[lo];
+        const int seg = a.items[li].seg;
+        const int g = seg % v.H, l = (seg / v.H) % v.L, b = seg / (v.H * v.L);
+        const size_t o = (size_t)b * v.NO + v.oidx[l * v.H + g];
+        const bool isv = c >= vpr;
+        x.cc = isv ? c - vpr : c;
+        x.pool = reinterpret_cast<uint4*>((char*)(isv ? v.slot_v : v.slot_k) + o * v.pool * row_bytes);
+        x.slot = a.fetch_slot[li * v.k + j];
+        x.dem = a.fetch_dem[li * v.k + j];
+        const int src = a.fetch_tok[li * v.k + j];
+        if (src >= 0) {
+            const size_t hb = (size_t)b * v.seq_stride + (size_t)l * v.layer_stride + (size_t)g * v.head_stride;
+            x.src = reinterpret_cast<const uint4*>((const char*)(fused || !isv ? v.host_k : v.host_v) + hb * esz) +
+                    (size_t)src * rvpr + (fused ? c : x.cc);
+        } else {
+            x.src = x.pool + (size_t)(-src - 1) * vpr + x.cc;
+        }
+        return x;
+    };
+    const long long step = (long long)gridDim.x * T * U;
+    auto issue = [&](long long base, int half) {
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const long long e = base + (long long)uu * T + threadIdx.x;
+            if (e < total) {
+                const Vec x = locate(e);
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + ((size_t)half * U + uu) * T + threadIdx.x));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(x.src) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    unsigned long long moved = 0;
+    long long base = (long long)blockIdx.x * T * U;
+    if (base < total) issue(base, 0);
+    for (int half = 0; base < total; base += step, half ^= 1) {
+        if (base + step < total) {
+            issue(base + step, half ^ 1);  // next batch's reads in flight during this batch's stores
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        // each thread stores the vectors it loaded (no barrier needed)
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const long long e = base + (long long)uu * T + threadIdx.x;
+            if (e < total) {
+                const Vec x = locate(e);
+                uint4* dp = x.pool + (size_t)x.slot * vpr + x.cc;
+                if (x.dem >= 0) x.pool[(size_t)x.dem * vpr + x.cc] = *dp;  // leaving row -> victim slot first
+                *dp = buf[((size_t)half * U + uu) * T + threadIdx.x];
+                moved += x.src < x.pool || x.src >= x.pool + (size_t)v.pool * vpr;  // host source
+            }
+        }
+    }
+    if (a.count_bytes) {
+        moved = __reduce_add_sync(0xffffffffu, (unsigned)moved);
+        if (lane == 0 && moved) atomicAdd(v.gathered_bytes, moved * 16ull);
+    }
+}
+
 // One launch per layer (prefill, and the serialised profiling graph).
 __global__ void __launch_bounds__(kGatherThreads) gather_engine_kernel(GatherEngineArgs a) {
     const int units = a.count[a.layer] * gather_units_per_item(a.v);
@@ -531,12 +742,52 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 // outstanding and wins (512K: +8%, 1M: +20%).
 // CLO_GATHER=lsu|tma forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
 void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stream) {
-    static const int mode = [] {  // 0 auto, 1 lsu, 2 tma
+    static const int mode = [] {  // 0 auto, 1 lsu, 2 tma, 3 wide
         const char* e = getenv("CLO_GATHER");
         if (!e || !*e) return 0;
         const std::string m(e);
-        return m == "lsu" ? 1 : (m == "tma" ? 2 : 0);
+        return m == "lsu" ? 1 : (m == "tma" ? 2 : (m == "wide" ? 3 : (m == "wide_smem" ? 4 : 0)));
     }();
+    if (mode == 4) {  // wide, rows in flight in shared memory
+        static const int shape = [] {  // CLO_GATHER_WIDE: 1: 512 x 8 (128 KiB/CTA), 2: 512 x 12 (192 KiB), 3: 1024 x 6 (192 KiB)
+            const char* e = getenv("CLO_GATHER_WIDE");
+            return e ? atoi(e) : 2;
+        }();
+        const int grid = ctas > 0 ? ctas : 16;
+        const size_t pref = ((size_t)a.items_cap + 1) * sizeof(int);
+#define CLO_WS(TT, UU)                                                                                        \
+    {                                                                                                         \
+        const size_t sm = 2 * (size_t)UU * TT * 16 + pref;                                                    \
+        cudaFuncSetAttribute(gather_wide_smem_kernel<TT, UU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+        gather_wide_smem_kernel<TT, UU><<<grid, TT, sm, stream>>>(a);                                          \
+    }
+        if (shape == 1) CLO_WS(512, 8) else if (shape == 3) CLO_WS(1024, 6) else CLO_WS(512, 12)
+#undef CLO_WS
+        return;
+    }
+    if (mode == 3) {
+        static const int reserve = [] {  // CLO_GATHER_RESERVE: KiB of shared memory per wide CTA
+            const char* e = getenv("CLO_GATHER_RESERVE");
+            return e && atoi(e) >= 0 ? atoi(e) : 160;
+        }();
+        const size_t sm = std::max<size_t>(((size_t)a.items_cap + 1) * sizeof(int), (size_t)reserve * 1024);
+        static const int shape = [] {  // CLO_GATHER_WIDE: threads x loads (1: 512x8, 2: 512x6, 3: 1024x4)
+            const char* e = getenv("CLO_GATHER_WIDE");
+            return e ? atoi(e) : 2;
+        }();
+        const int grid = ctas > 0 ? ctas : 16;
+        if (shape == 1) {
+            cudaFuncSetAttribute(gather_wide_kernel<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            gather_wide_kernel<512, 8><<<grid, 512, sm, stream>>>(a);
+        } else if (shape == 3) {
+            cudaFuncSetAttribute(gather_wide_kernel<1024, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            gather_wide_kernel<1024, 4><<<grid, 1024, sm, stream>>>(a);
+        } else {
+            cudaFuncSetAttribute(gather_wide_kernel<512, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            gather_wide_kernel<512, 6><<<grid, 512, sm, stream>>>(a);
+        }
+        return;
+    }
     static const int2 shape = [] {
         int2 r{1, 1};
         if (const char* e = getenv("CLO_GATHER_TMA_SHAPE")) {
