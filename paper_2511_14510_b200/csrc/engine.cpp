@@ -162,9 +162,11 @@ Engine::~Engine() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_join2_) cudaEventDestroy(ev_join2_);
+    if (ev_join3_) cudaEventDestroy(ev_join3_);
     if (ev_step_) cudaEventDestroy(ev_step_);
     if (s_main_) cudaStreamDestroy(s_main_);
     if (s_pref_) cudaStreamDestroy(s_pref_);
+    if (s_pref2_) cudaStreamDestroy(s_pref2_);
     if (s_xfer_) cudaStreamDestroy(s_xfer_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
     for (int i = 0; i < 2; ++i) {
@@ -347,12 +349,21 @@ void Engine::allocate() {
     for (auto& b : d_in_) b.alloc(2 * sizeof(float) * B * L * HQ * d + 2 * esz * B * L * H * d, false);
     d_out_.alloc(sizeof(float) * B * L * HQ * d, false);
 
-    for (int i = 0; i < 2; ++i) {
+    {
+        // CLO_SEL_STREAMS=2: even and odd layers' selections on two streams
+        // (experiment, neutral on B200); default one selection stream
+        const char* e = getenv("CLO_SEL_STREAMS");
+        sel_streams_ = e && atoi(e) == 2 ? 2 : 1;
+    }
+    for (int i = 0; i < 3; ++i) {
+        if (i == 2 && sel_streams_ < 2) break;
         SelScratch& sc = scratch_[i];
         auto& bufs = scratch_bufs_[i];
         const size_t items = (size_t)B * H;
-        bufs[0].alloc(sizeof(int) * L);
-        bufs[1].alloc(sizeof(SelItem) * items * L);  // per-layer work lists
+        if (i < 2) {
+            bufs[0].alloc(sizeof(int) * L);
+            bufs[1].alloc(sizeof(SelItem) * items * L);  // per-layer work lists
+        }
         bufs[2].alloc(sizeof(double) * items * m * d);
         bufs[3].alloc(sizeof(uint64_t) * items * m * words_);
         if (cfg_.retriever == CLO_RETRIEVER_SIGN_HASH)
@@ -366,15 +377,15 @@ void Engine::allocate() {
         bufs[10].alloc(sizeof(int) * items);
         bufs[11].alloc(sizeof(uint32_t) * items * 256);
         bufs[17].alloc(sizeof(int) * 2 * items);  // chained-stage chunk counters (zero between launches)
-        if (i == 1) {  // offloaded heads: new selections + per-layer fetch lists
-            bufs[12].alloc(sizeof(int32_t) * items * k, false);
+        if (i >= 1) bufs[12].alloc(sizeof(int32_t) * items * k, false);  // offloaded: new selections
+        if (i == 1) {  // per-layer work and fetch lists (shared by both selection streams)
             bufs[13].alloc(sizeof(int32_t) * L * items * k, false);
             bufs[14].alloc(sizeof(int32_t) * L * items * k, false);
             bufs[15].alloc(sizeof(int) * L * items);
             bufs[16].alloc(sizeof(int32_t) * L * items * k, false);
         }
-        sc.count = bufs[0].as<int>();
-        sc.items = bufs[1].as<SelItem>();
+        sc.count = i == 2 ? scratch_[1].count : bufs[0].as<int>();
+        sc.items = i == 2 ? scratch_[1].items : bufs[1].as<SelItem>();
         sc.q64 = bufs[2].as<double>();
         sc.qbits = bufs[3].as<uint64_t>();
         sc.key16 = bufs[4].as<uint16_t>();
@@ -386,10 +397,11 @@ void Engine::allocate() {
         sc.need = bufs[10].as<int>();
         sc.radix_hist = bufs[11].as<uint32_t>();
         sc.sel = bufs[12].as<int32_t>();
-        sc.fetch_tok = bufs[13].as<int32_t>();
-        sc.fetch_slot = bufs[14].as<int32_t>();
-        sc.fetch_count = bufs[15].as<int>();
-        sc.fetch_dem = bufs[16].as<int32_t>();
+        const auto& lists = scratch_bufs_[i == 2 ? 1 : i];
+        sc.fetch_tok = lists[13].as<int32_t>();
+        sc.fetch_slot = lists[14].as<int32_t>();
+        sc.fetch_count = lists[15].as<int>();
+        sc.fetch_dem = lists[16].as<int32_t>();
         sc.item_done = bufs[17].as<int>();
     }
 
@@ -402,6 +414,7 @@ void Engine::allocate() {
         CLO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         const int p = e && std::string(e) == "high" ? hi : (e && std::string(e) == "mid" ? (lo + hi) / 2 : lo);
         CLO_CUDA(cudaStreamCreateWithPriority(&s_pref_, cudaStreamNonBlocking, p));
+        if (sel_streams_ > 1) CLO_CUDA(cudaStreamCreateWithPriority(&s_pref2_, cudaStreamNonBlocking, p));
     }
     // The transfer stream gets the highest priority: when attention CTAs
     // retire, the next layer's gather CTAs are scheduled first so the PCIe
@@ -412,6 +425,7 @@ void Engine::allocate() {
     CLO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     CLO_CUDA(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
+    CLO_CUDA(cudaEventCreateWithFlags(&ev_join3_, cudaEventDisableTiming));
     ev_attn_.resize(L);
     ev_pref_.resize(L);
     ev_sel_.resize(L);
@@ -538,7 +552,7 @@ EngineView Engine::view() const {
 
 SelArgs Engine::sel_args(int which, int layer) const {
     const clo_model_shape& s = cfg_.shape;
-    const SelScratch& sc = scratch_[which];
+    const SelScratch& sc = which ? off_scratch(layer) : scratch_[0];
     SelArgs a{};
     a.items = sc.items + (size_t)layer * cfg_.batch * s.num_kv_heads;
     a.count = sc.count + layer;
@@ -642,7 +656,7 @@ int Engine::chained_select() const {
 }
 
 ReconcileArgs Engine::reconcile_args(int layer, int fresh) const {
-    const SelScratch& sc = scratch_[1];
+    const SelScratch& sc = off_scratch(layer);
     const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
     ReconcileArgs ra{};
     ra.v = view();
@@ -678,7 +692,7 @@ void Engine::enqueue_select(int which, int layer, cudaStream_t st, bool with_rec
 void Engine::enqueue_prepare(int which, int layer, int mode, int kind, cudaStream_t st) {
     PrepareArgs pa{};
     pa.v = view();
-    pa.s = scratch_[which];
+    pa.s = which ? off_scratch(layer) : scratch_[0];
     pa.s.items += (size_t)layer * cfg_.batch * cfg_.shape.num_kv_heads;
     pa.layer = layer;
     pa.mode = mode;
@@ -711,13 +725,13 @@ void Engine::enqueue_fused_select(int layer, cudaStream_t st) {
     const size_t items = (size_t)cfg_.batch * cfg_.shape.num_kv_heads;
     FusedSelectArgs f{};
     f.prep.v = view();
-    f.prep.s = scratch_[1];
+    f.prep.s = off_scratch(layer);
     f.prep.s.items += (size_t)layer * items;
     f.prep.layer = layer;
     f.prep.mode = kPrepDecode;
     f.prep.kind = kKindOffloaded;
     f.sel = sel_args(1, layer);
-    const SelScratch& sc = scratch_[1];
+    const SelScratch& sc = off_scratch(layer);
     f.rec.v = f.prep.v;
     f.rec.items = sc.items + (size_t)layer * items;
     f.rec.count = sc.count;
@@ -1009,7 +1023,15 @@ void Engine::capture_graph(int mode) {
     // The instrumented (profiled) graph serialises everything on one stream so
     // each kernel's event-bracketed time is its own, not time spent queued
     // behind the other streams (the share of the step, like an ncu launch list).
-    cudaStream_t s_pref = profiled ? s_main_ : s_pref_;
+    // CLO_SEL_STREAMS=2 (experiment): even layers' selections on one stream,
+    // odd layers' on another, each with its own stage intermediates
+    // (off_scratch), so the chain in front of gather(l) no longer queues
+    // behind layer l-1's chain. On B200 it halves the link's wait for fetch
+    // lists but the overlapping selection kernels slow the gathers and
+    // attention by as much (1595 vs 1595 tokens/s, profiles/r2/experiments.jsonl).
+    const bool dual = !profiled && !flags && sel_streams_ > 1;
+    cudaStream_t s_pref_a = profiled ? s_main_ : s_pref_;
+    cudaStream_t s_pref_b = dual ? s_pref2_ : s_pref_a;
     cudaStream_t s_xfer = profiled ? s_main_ : s_xfer_;
     CLO_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeThreadLocal));
     if (mode == kGraphTimeline) {
@@ -1018,7 +1040,8 @@ void Engine::capture_graph(int mode) {
     }
     CLO_CUDA(cudaEventRecord(ev_fork_, s_main_));
     if (!profiled) {
-        CLO_CUDA(cudaStreamWaitEvent(s_pref, ev_fork_, 0));
+        CLO_CUDA(cudaStreamWaitEvent(s_pref_a, ev_fork_, 0));
+        if (dual) CLO_CUDA(cudaStreamWaitEvent(s_pref_b, ev_fork_, 0));
         CLO_CUDA(cudaStreamWaitEvent(s_xfer, ev_fork_, 0));
         // one persistent transfer kernel per step streams every offloaded
         // layer's fetch list as soon as the selection stream publishes it
@@ -1029,6 +1052,7 @@ void Engine::capture_graph(int mode) {
         }
     }
     for (int l = 0; l < L; ++l) {
+        cudaStream_t s_pref = (l & 1) ? s_pref_b : s_pref_a;
         if (layer_has_off_[l]) {
             // The lookup/selection/transfer of layer l uses approximate queries,
             // available once layer l-1 starts, i.e. after attention(l-2):
@@ -1076,8 +1100,12 @@ void Engine::capture_graph(int mode) {
         CLO_CUDA(cudaEventRecord(ev_attn_[l], s_main_));
     }
     if (!profiled) {
-        CLO_CUDA(cudaEventRecord(ev_join_, s_pref));
+        CLO_CUDA(cudaEventRecord(ev_join_, s_pref_a));
         CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
+        if (dual) {
+            CLO_CUDA(cudaEventRecord(ev_join3_, s_pref_b));
+            CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join3_, 0));
+        }
         CLO_CUDA(cudaEventRecord(ev_join2_, s_xfer));
         CLO_CUDA(cudaStreamWaitEvent(s_main_, ev_join2_, 0));
     }

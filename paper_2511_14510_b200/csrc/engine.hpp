@@ -119,11 +119,16 @@ class Engine {
     std::array<cudaEvent_t, 2> ev_in_{}, ev_free_{};
     std::array<bool, 2> in_used_{};
     int pending_free_ = -1;  // slot whose consumer graph is being launched
-    std::array<SelScratch, 2> scratch_{};  // 0: compute stream (persistent), 1: prefetch stream
-    std::array<std::array<DevBuf, 18>, 2> scratch_bufs_;
+    // 0: compute stream (persistent heads); 1, 2: the two selection streams
+    // (offloaded heads of even / odd layers). 2 owns only the per-stage
+    // intermediates; its per-layer work and fetch lists alias 1's.
+    std::array<SelScratch, 3> scratch_{};
+    std::array<std::array<DevBuf, 18>, 3> scratch_bufs_;
+    int sel_streams_ = 1;  // CLO_SEL_STREAMS: selection streams (layers by parity)
+    const SelScratch& off_scratch(int layer) const { return scratch_[sel_streams_ > 1 && (layer & 1) ? 2 : 1]; }
 
-    cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_xfer_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr;
+    cudaStream_t s_main_ = nullptr, s_pref_ = nullptr, s_pref2_ = nullptr, s_xfer_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_join2_ = nullptr, ev_join3_ = nullptr;
     std::vector<cudaEvent_t> ev_attn_, ev_pref_, ev_sel_;
     std::array<cudaGraph_t, kGraphModes> graphs_{};
     std::array<cudaGraphExec_t, kGraphModes> execs_{};
