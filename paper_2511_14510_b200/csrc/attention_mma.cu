@@ -32,6 +32,7 @@
 //     (split hi/lo on the fly), ldmatrix.trans V, m16n8k16 over d/8 dim tiles;
 //   * per-warp partials merge in a small combine kernel (flash decoding).
 // Each KV row is read from HBM exactly once for all m query heads.
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -112,6 +113,7 @@ struct MmaPlan {
     int W;       // warps per CTA (each warp flushes its own partials)
     int single;  // G = c * B*H: CTA j serves piece j % c of head j / c (warps merge in shared memory)
     int c;       // CTAs per head when single
+    int cluster; // single, c > 1: a head's c CTAs are one thread-block cluster and merge over DSMEM
     int seg[kMaxCtas + 1];  // segment starts S_j = j*T/G (T < 2^31)
 };
 
@@ -602,6 +604,7 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
     // last of the head's c CTAs merges them in piece order.
     __syncthreads();  // every warp is done with its ring
     float* red = reinterpret_cast<float*>(smem);  // [kWarpsM][M][D + 2]
+    float* cpart = red + (size_t)kWarpsM * M * (D + 2);  // [M][D + 4] this CTA's partial (cluster merge)
     {
         float lsum = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
@@ -635,6 +638,13 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         }
         if (pl.c == 1) {
             emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+        } else if (pl.cluster) {  // this CTA's partial stays in its shared memory
+            float* pp = cpart + (size_t)q * (D + 4);
+            pp[e] = a;
+            if (e == 0) {
+                pp[D] = gm;
+                pp[D + 1] = den;
+            }
         } else {
             float* pp = ph + ((size_t)piece * M + q) * (D + 4);
             __stcg(pp + e, a);
@@ -644,7 +654,32 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
             }
         }
     }
-    if (pl.c > 1) {
+    if (pl.c > 1 && pl.cluster) {
+        // The head's c CTAs form one cluster (rank = piece): rank 0 merges
+        // the c partials in piece order over DSMEM (the same arithmetic and
+        // order as the global-memory merge below), without a global fence —
+        // a gpu-scope fence waits for every host read the concurrent gather
+        // has queued (profiles/r2/pdl_exit_probe.txt), a cluster barrier does not.
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        if (piece == 0) {
+            for (int x = threadIdx.x; x < M * D; x += kWarpsM * 32) {
+                const int q = x / D, e = x - q * D;
+                float gm = -CUDART_INF_F;
+                for (int cc = 0; cc < pl.c; ++cc) gm = fmaxf(gm, cl.map_shared_rank(cpart, cc)[(size_t)q * (D + 4) + D]);
+                float a = 0.f, den = 0.f;
+                for (int cc = 0; cc < pl.c; ++cc) {
+                    const float* pp = cl.map_shared_rank(cpart, cc) + (size_t)q * (D + 4);
+                    const float cw = wexp(pp[D], gm);
+                    a += pp[e] * cw;
+                    den += pp[D + 1] * cw;
+                }
+                emit_head_output(v, t, hb, l, g * M + q, e, a / den);
+            }
+        }
+        cl.sync();  // the other CTAs' shared memory stays live until rank 0 has read it
+    } else if (pl.c > 1) {
         __shared__ int s_last_cta;
         __threadfence();
         __syncthreads();
@@ -668,6 +703,14 @@ __global__ void __maxnreg__(kRegCap) attn_mma_stream_kernel(const __grid_constan
         if (threadIdx.x == 0) v.attn_count[h] = 0;
     }
     signal_head_output(v, l);
+}
+
+bool attn_cluster_enabled() {  // CLO_ATTN_CLUSTER=0: c > 1 CTAs per head merge through global memory
+    static const bool on = [] {
+        const char* e = getenv("CLO_ATTN_CLUSTER");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 MmaPlan make_plan(const EngineView& v, int W, int ctas_per_sm, int TM) {
@@ -742,7 +785,31 @@ void launch_mma_shape_rc(const EngineView& v, int layer, cudaStream_t stream) {
         vv.tmap_k = v.tmap_k32;
         vv.tmap_v = v.tmap_v32;
     }
-    attn_mma_stream_kernel<D, M, W, S, C, TM, RC><<<pl.G, W * 32, sm, stream>>>(vv, layer, pl, v.attn_part);
+    auto kern = attn_mma_stream_kernel<D, M, W, S, C, TM, RC>;
+    if (pl.single && pl.c > 1 && pl.c <= 16 && attn_cluster_enabled()) {
+        // one cluster per head (DSMEM merge) when every cluster fits at once
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(pl.G);
+        cfg.blockDim = dim3(W * 32);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = pl.c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (pl.c > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters * pl.c >= pl.G) {
+            MmaPlan pc = pl;
+            pc.cluster = 1;
+            if (cudaLaunchKernelEx(&cfg, kern, vv, layer, pc, v.attn_part) == cudaSuccess) return;
+        }
+        cudaGetLastError();  // not co-schedulable here: the global-memory merge
+    }
+    kern<<<pl.G, W * 32, sm, stream>>>(vv, layer, pl, v.attn_part);
 }
 
 // Register cap: CLO_ATTN_REGCAP=184 lets an 8-warp CTA share its SM with a

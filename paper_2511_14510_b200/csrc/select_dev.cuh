@@ -9,6 +9,38 @@ namespace clo {
 
 __device__ __forceinline__ int num_chunks(int n) { return (n + kScoreChunk - 1) / kScoreChunk; }
 
+// Register-cached variant bound: chunks per warp x 32-bin blocks per lane.
+constexpr int kThrCpw = 4, kThrBpl = 9;
+
+// T from the item's bin totals (tot, shared memory), by warp 0: walk bins from
+// the top in blocks of 32 with suffix sums by warp scan. Writes sts.
+__device__ __forceinline__ void threshold_walk(const SelArgs& a, const uint32_t* tot, int* sts) {
+    const int lane = threadIdx.x & 31;
+    int running = 0, T = -1, gtT = 0;
+    for (int top = a.nb - 1; top >= 0 && T < 0; top -= 32) {
+        const int b = top - lane;
+        int v = b >= 0 ? (int)tot[b] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= a.k);
+        if (hit) {
+            const int first = __ffs(hit) - 1;
+            const int excl = __shfl_sync(0xffffffffu, incl - v, first);
+            T = top - first;
+            gtT = running + excl;
+        }
+        running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+        sts[0] = T;
+        sts[1] = gtT;
+    }
+}
+
 // Per item: T = k-th largest S (ties resolved later by index), then each
 // chunk's output offset and how many of its S == T ties it keeps.
 // Whole CTA; smem = nb + 2*max_chunks words, sts = 2 ints. Ends with __syncthreads().
@@ -16,74 +48,99 @@ __device__ __forceinline__ void threshold_item(const SelArgs& a, int item, uint3
     uint32_t* tot = smem;                               // [nb]
     int* gt = reinterpret_cast<int*>(smem + a.nb);      // [max_chunks]
     int* eq = gt + a.max_chunks;                        // [max_chunks]
-    int& sT = sts[0];
-    int& sGt = sts[1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     {
         const SelItem it = a.items[item];
         const int nch = num_chunks(it.n);
         const uint32_t* hist = a.chunk_hist + (size_t)item * a.max_chunks * a.nb;
-        if (nch <= 64) {  // one thread per bin walks the chunks
-            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
-                uint32_t s = 0;
-#pragma unroll 8
-                for (int c = 0; c < nch; ++c) s += hist[(size_t)c * a.nb + b];
-                tot[b] = s;
+        const int nbb = (a.nb + 31) / 32;
+        if (nch <= kThrCpw * nwarps && nbb <= kThrBpl) {
+            // Warp w holds chunks w, w + nwarps, ... (up to 4) x all bins in
+            // registers: every histogram load of the item is issued at once (one
+            // L2 round trip instead of one per 32-bin block), and the per-chunk
+            // counts above / at T come from the same registers.
+            uint32_t hv[kThrCpw][kThrBpl];
+#pragma unroll
+            for (int ci = 0; ci < kThrCpw; ++ci) {
+                const int c = warp + ci * nwarps;
+#pragma unroll
+                for (int bb = 0; bb < kThrBpl; ++bb) {
+                    const int b = bb * 32 + lane;
+                    hv[ci][bb] = c < nch && b < a.nb ? __ldcg(hist + (size_t)c * a.nb + b) : 0u;
+                }
             }
-        } else {  // long items: warp w sums chunks w, w + nwarps, ... (coalesced bin rows)
             for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
             __syncthreads();
-            for (int b0 = 0; b0 < a.nb; b0 += 32) {
-                const int b = b0 + lane;
-                if (b < a.nb) {
+#pragma unroll
+            for (int bb = 0; bb < kThrBpl; ++bb) {
+                uint32_t sum = 0;
+#pragma unroll
+                for (int ci = 0; ci < kThrCpw; ++ci) sum += hv[ci][bb];
+                if (sum) atomicAdd(&tot[bb * 32 + lane], sum);
+            }
+            __syncthreads();
+            if (warp == 0) threshold_walk(a, tot, sts);
+            __syncthreads();
+            const int T = sts[0];
+#pragma unroll
+            for (int ci = 0; ci < kThrCpw; ++ci) {
+                const int c = warp + ci * nwarps;
+                int g = 0, e = 0;
+#pragma unroll
+                for (int bb = 0; bb < kThrBpl; ++bb) {
+                    const int b = bb * 32 + lane;
+                    g += b > T ? (int)hv[ci][bb] : 0;
+                    e += b == T ? (int)hv[ci][bb] : 0;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
+                    e += __shfl_xor_sync(0xffffffffu, e, o);
+                }
+                if (lane == 0 && c < nch) {
+                    gt[c] = g;
+                    eq[c] = e;
+                }
+            }
+        } else {
+            if (nch <= 64) {  // one thread per bin walks the chunks
+                for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
                     uint32_t s = 0;
+#pragma unroll 8
+                    for (int c = 0; c < nch; ++c) s += hist[(size_t)c * a.nb + b];
+                    tot[b] = s;
+                }
+            } else {  // long items: warp w sums chunks w, w + nwarps, ... (coalesced bin rows)
+                for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
+                __syncthreads();
+                for (int b0 = 0; b0 < a.nb; b0 += 32) {
+                    const int b = b0 + lane;
+                    if (b < a.nb) {
+                        uint32_t s = 0;
 #pragma unroll 4
-                    for (int c = warp; c < nch; c += nwarps) s += hist[(size_t)c * a.nb + b];
-                    if (s) atomicAdd(&tot[b], s);
+                        for (int c = warp; c < nch; c += nwarps) s += hist[(size_t)c * a.nb + b];
+                        if (s) atomicAdd(&tot[b], s);
+                    }
                 }
             }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            // Walk bins from the top in blocks of 32: suffix sums by warp scan.
-            int running = 0, T = -1, gtT = 0;
-            for (int top = a.nb - 1; top >= 0 && T < 0; top -= 32) {
-                const int b = top - lane;
-                int v = b >= 0 ? (int)tot[b] : 0;
-                int incl = v;
+            __syncthreads();
+            if (warp == 0) threshold_walk(a, tot, sts);
+            __syncthreads();
+            const int T = sts[0];
+            for (int c = warp; c < nch; c += nwarps) {
+                const uint32_t* h = hist + (size_t)c * a.nb;
+                int g = 0;
+                for (int b = T + 1 + lane; b < a.nb; b += 32) g += h[b];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
+                for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+                if (lane == 0) {
+                    gt[c] = g;
+                    eq[c] = h[T];
                 }
-                const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= a.k);
-                if (hit) {
-                    const int first = __ffs(hit) - 1;
-                    const int excl = __shfl_sync(0xffffffffu, incl - v, first);
-                    T = top - first;
-                    gtT = running + excl;
-                }
-                running += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) {
-                sT = T;
-                sGt = gtT;
             }
         }
         __syncthreads();
-        const int T = sT, need_eq = a.k - sGt;
-        for (int c = warp; c < nch; c += nwarps) {
-            const uint32_t* h = hist + (size_t)c * a.nb;
-            int g = 0;
-            for (int b = T + 1 + lane; b < a.nb; b += 32) g += h[b];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
-            if (lane == 0) {
-                gt[c] = g;
-                eq[c] = h[T];
-            }
-        }
-        __syncthreads();
+        const int need_eq = a.k - sts[1];
         if (warp == 0) {
             int base_run = 0, eq_run = 0;
             for (int c0 = 0; c0 < nch; c0 += 32) {
@@ -112,7 +169,7 @@ __device__ __forceinline__ void threshold_item(const SelArgs& a, int item, uint3
                 eq_run += __shfl_sync(0xffffffffu, ie, 31);
             }
             if (lane == 0) {
-                a.thresh[item] = (uint64_t)T;
+                a.thresh[item] = (uint64_t)sts[0];
                 a.need[item] = need_eq;
             }
         }

@@ -87,6 +87,16 @@ def test_gqa_groups_of_five_and_d128(oracle):
     run_and_compare(case, oracle)
 
 
+@pytest.mark.parametrize("batch,hkv", [(4, 8), (2, 4)])
+def test_attention_cluster_merge(oracle, batch, hkv):
+    # B*H = 32 / 8 heads on 148 SMs: c = 4 / 18 CTAs per head. c = 4 runs as
+    # one thread-block cluster per head with the DSMEM merge; c = 18 (> 16)
+    # keeps the global-memory merge. Both against the oracle.
+    case = make_case(L=2, hq=4 * hkv, hkv=hkv, d=128, n_prompt=700, steps=4, k=64, kv_dtype="bf16",
+                     sink=4, recent=32, batch=batch)
+    run_and_compare(case, oracle)
+
+
 def test_cache_state_json_matches_oracle_layout(oracle):
     case = make_case(steps=8)
     g, o, _ = run_and_compare(case, oracle)
