@@ -10,7 +10,12 @@ namespace clo {
 __device__ __forceinline__ int num_chunks(int n) { return (n + kScoreChunk - 1) / kScoreChunk; }
 
 // Register-cached variant bound: chunks per warp x 32-bin blocks per lane.
-constexpr int kThrCpw = 4, kThrBpl = 9;
+// A chunk's bin counts are <= kScoreChunk < 2^16, so two blocks share a
+// register (low / high half): 5 chunks x 5 registers per lane cover 512K-token
+// items (129 chunks) with 1024 threads and 256-bit hashes (nb = 257 <= 320)
+// without spilling under the 64-register cap; longer items take the loop.
+constexpr int kThrCpw = 5, kThrBpl = 10;
+static_assert(kScoreChunk < 65536, "u16 bin counts");
 
 // T from the item's bin totals (tot, shared memory), by warp 0: walk bins from
 // the top in blocks of 32 with suffix sums by warp scan. Writes sts.
@@ -59,23 +64,26 @@ __device__ __forceinline__ void threshold_item(const SelArgs& a, int item, uint3
             // registers: every histogram load of the item is issued at once (one
             // L2 round trip instead of one per 32-bin block), and the per-chunk
             // counts above / at T come from the same registers.
-            uint32_t hv[kThrCpw][kThrBpl];
+            uint32_t hv[kThrCpw][kThrBpl / 2];
 #pragma unroll
             for (int ci = 0; ci < kThrCpw; ++ci) {
                 const int c = warp + ci * nwarps;
 #pragma unroll
-                for (int bb = 0; bb < kThrBpl; ++bb) {
-                    const int b = bb * 32 + lane;
-                    hv[ci][bb] = c < nch && b < a.nb ? __ldcg(hist + (size_t)c * a.nb + b) : 0u;
+                for (int bp = 0; bp < kThrBpl / 2; ++bp) {
+                    const int b0 = 2 * bp * 32 + lane, b1 = b0 + 32;
+                    const uint32_t lo = c < nch && b0 < a.nb ? __ldcg(hist + (size_t)c * a.nb + b0) : 0u;
+                    const uint32_t hi = c < nch && b1 < a.nb ? __ldcg(hist + (size_t)c * a.nb + b1) : 0u;
+                    hv[ci][bp] = lo | (hi << 16);
                 }
             }
+            auto bin = [&](int ci, int bb) -> uint32_t { return (hv[ci][bb >> 1] >> ((bb & 1) * 16)) & 0xFFFFu; };
             for (int b = threadIdx.x; b < a.nb; b += blockDim.x) tot[b] = 0;
             __syncthreads();
 #pragma unroll
             for (int bb = 0; bb < kThrBpl; ++bb) {
                 uint32_t sum = 0;
 #pragma unroll
-                for (int ci = 0; ci < kThrCpw; ++ci) sum += hv[ci][bb];
+                for (int ci = 0; ci < kThrCpw; ++ci) sum += bin(ci, bb);
                 if (sum) atomicAdd(&tot[bb * 32 + lane], sum);
             }
             __syncthreads();
@@ -89,8 +97,8 @@ __device__ __forceinline__ void threshold_item(const SelArgs& a, int item, uint3
 #pragma unroll
                 for (int bb = 0; bb < kThrBpl; ++bb) {
                     const int b = bb * 32 + lane;
-                    g += b > T ? (int)hv[ci][bb] : 0;
-                    e += b == T ? (int)hv[ci][bb] : 0;
+                    g += b > T ? (int)bin(ci, bb) : 0;
+                    e += b == T ? (int)bin(ci, bb) : 0;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
