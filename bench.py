@@ -112,6 +112,7 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device, self.rows, self.proc = device, [], None
+        self.window = None  # (t0, t1) of the timed region, time.monotonic()
 
     def __enter__(self):
         try:
@@ -127,7 +128,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def wait_first(self, timeout=3.0):
+        """nvidia-smi needs ~0.1-0.3 s to its first sample: started before the
+        warm-up, the sampler is live when the timed region begins."""
+        end = time.monotonic() + timeout
+        while self.proc and not self.rows and time.monotonic() < end:
+            time.sleep(0.01)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -135,13 +143,23 @@ class ClockSampler:
             self.proc.wait(timeout=5)
 
     def summary(self):
-        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        # samples inside the timed region; a region shorter than the 100 ms
+        # sampling period (configs[0]: ~25 ms) takes the samples of the
+        # warm-up + timed region instead and says so
+        rows, window = [r for _, r in self.rows], "timed region"
+        if self.window:
+            inside = [r for t, r in self.rows if self.window[0] <= t <= self.window[1] + 0.05]
+            if inside:
+                rows = inside
+            else:
+                window = "warm-up + timed region (timed region shorter than the 100 ms sampling period)"
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4)
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4)
                           if r[5 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "window": window}
 
 
 def measured_peaks():
@@ -497,6 +515,8 @@ def run_ours(args):
         return float(tt.item())
 
     # ---- warm-up + timed region (inputs resident in HBM) -------------------
+    clocks = ClockSampler(local).__enter__()  # live (first sample in) before the timed region
+    clocks.wait_first()
     for _ in range(W):
         step_dev()
     m0 = eng.metrics()
@@ -504,13 +524,15 @@ def run_ours(args):
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for i in range(K):
-            step_dev()
-            step_ev[i].record(stream)
-        ev1.record(stream)
-        barrier()
+    t_region0 = time.monotonic()
+    ev0.record(stream)
+    for i in range(K):
+        step_dev()
+        step_ev[i].record(stream)
+    ev1.record(stream)
+    barrier()
+    clocks.window = (t_region0, time.monotonic())
+    clocks.__exit__(None, None, None)
     step_ms = [ev0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, K)]
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = eng.kernel_launches() - launches0
