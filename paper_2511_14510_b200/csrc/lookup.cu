@@ -53,9 +53,15 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
     __shared__ LookupShared sh;
     __shared__ __align__(8) uint64_t bar;
 
+    // code word `rank`'s P slice: its bulk copy is issued first and lands
+    // while rank 0 stages and decides (the slice depends on (l, g, rank) only)
+    const double* slice = v.proj_w + ((size_t)lg * v.words + rank) * v.d * 64;
     if (threadIdx.x == 0) {
         sh.selected = 0;
-        if (nr > 1) bulk::mbar_init(&bar);
+        if (nr > 1) {
+            bulk::mbar_init(&bar);
+            bulk::load_async(ps, slice, (uint32_t)v.d * 64 * 8, &bar);
+        }
     }
     // queries (every rank hashes them) and, on rank 0, the labels: one round trip
     lookup_stage(a, b, g, rank == 0, q, lab_s);
@@ -79,13 +85,10 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(PrepareArgs a) {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     CLO_PROBE_T(tp, 3)
+    if (nr > 1) bulk::wait(&bar, 0);  // no CTA exits with its slice copy in flight
     if (!selected) return;
     // code word `rank` of the m query sign-hashes
-    const double* slice = v.proj_w + ((size_t)lg * v.words + rank) * v.d * 64;
-    if (nr > 1) {
-        if (threadIdx.x == 0) bulk::load_async(ps, slice, (uint32_t)v.d * 64 * 8, &bar);
-        bulk::wait(&bar, 0);
-    } else {
+    if (nr == 1) {
         for (int i = threadIdx.x; i < v.d * 64; i += blockDim.x) ps[i] = slice[i];
         __syncthreads();
     }

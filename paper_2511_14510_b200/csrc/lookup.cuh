@@ -212,12 +212,18 @@ __device__ __forceinline__ void lookup_stage(const PrepareArgs& a, int b, int g,
     const float* qsrc = (prefill || pers) ? v.desc->true_q : v.desc->approx_q;
     const size_t qoff = (((size_t)b * v.L + l) * v.HQ + (size_t)g * v.m) * v.d;
     const double* lab = v.labels + qoff;
+    // One round trip: the finiteness flag is raised once after the loop (a
+    // conditional atomic inside it kept the compiler from issuing the next
+    // iteration's loads early: rank 0 spent 8-12 us here in the step graph,
+    // profiles/r2/prepare_phase_probe_128ctas.txt, the other ranks 1.6 us).
+    bool bad = false;
     for (int i = threadIdx.x; i < v.m * v.d; i += blockDim.x) {
-        const float x = qsrc[qoff + i];
-        if (check && !isfinite(x)) raise_err(v.err, kErrNonFiniteQuery);
+        const float x = __ldg(qsrc + qoff + i);
+        bad |= !isfinite(x);
         q[i] = (double)x;
         if (check && lookup) lab_s[i] = lab[i];
     }
+    if (check && bad) raise_err(v.err, kErrNonFiniteQuery);
     __syncthreads();
 }
 
