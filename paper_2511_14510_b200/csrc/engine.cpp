@@ -680,8 +680,7 @@ void Engine::enqueue_select(int which, int layer, cudaStream_t st, bool with_rec
         // decode, offloaded heads, chained stages: the compaction kernel also
         // reconciles each item's entry (one launch instead of two)
         const ReconcileArgs ra = reconcile_args(layer, 0);
-        launch_select_signhash(a, st, with_reconcile && chained_select() == 2 ? &ra : nullptr);
-        launches_ += a.item_done ? 2 : 3;
+        launches_ += launch_select_signhash(a, st, with_reconcile && chained_select() == 2 ? &ra : nullptr);
     } else {
         launch_select_exact(a, st);
         launches_ += 21;

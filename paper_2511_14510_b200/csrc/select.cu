@@ -295,6 +295,22 @@ __global__ void __launch_bounds__(kScoreThreads) compact_kernel(SelArgs a) {
     for (int u = blockIdx.x; u < units; u += gridDim.x) compact_unit<KeyT>(a, u / a.max_chunks, u % a.max_chunks, s_gt, s_eq);
 }
 
+// Compaction with the threshold recomputed per CTA (chunk_quota): sign-hash
+// items of <= 64 chunks, one launch instead of threshold + compaction.
+__global__ void __launch_bounds__(kScoreThreads) compact_quota_kernel(SelArgs a) {
+    __shared__ int s_gt[kWarps], s_eq[kWarps], s_sts[2], s_red[kWarps];
+    __shared__ uint32_t s_tot[kMaxBins], s_pre[kMaxBins], s_cur[kMaxBins];
+    const int units = *a.count * a.max_chunks;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = u / a.max_chunks, chunk = u % a.max_chunks;
+        const SelItem it = a.items[item];
+        if (chunk * kScoreChunk >= it.n) continue;
+        int T, take, base;
+        chunk_quota(a, item, chunk, num_chunks(it.n), s_tot, s_pre, s_cur, s_sts, s_red, T, take, base);
+        compact_body<uint16_t>(a, it, item, chunk, (uint16_t)T, take, base, s_gt, s_eq);
+    }
+}
+
 // Compaction of the offloaded heads whose CTA finishing an item's last chunk
 // then reconciles that item's entry (reconcile_kernel's work, reconcile.cuh):
 // the fetch list is ready when this kernel ends, one launch earlier.
@@ -526,7 +542,7 @@ void launch_score_tma(const SelArgs& a, int grid, size_t sm, int agg, cudaStream
     }
 }
 
-void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec) {
+int launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec) {
     const size_t sm_score = (size_t)kWarps * a.nb * 4 + 8 + (size_t)a.m * a.words * 8;
     static const bool tma = [] {  // CLO_SCORE=lsu: the register-load kernel
         const char* e = getenv("CLO_SCORE");
@@ -561,6 +577,14 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const Reconci
     // one CTA per item (the kernels grid-stride over *count <= max_items)
     const int items_grid = a.max_items > 0 ? (a.max_items < 1024 ? a.max_items : 1024) : (a.grid < 1024 ? a.grid : 1024);
     const bool tma_chained = tma && a.item_done;  // the score kernel's last chunk per item ran the threshold
+    static const bool quota = [] {  // CLO_COMPACT_QUOTA=0: separate threshold launch
+        const char* e = getenv("CLO_COMPACT_QUOTA");
+        return !(e && e[0] == '0');
+    }();
+    if (quota && !tma_chained && !rec && a.max_chunks <= 64 && a.nb <= kMaxBins) {
+        compact_quota_kernel<<<a.grid, kScoreThreads, 0, stream>>>(a);
+        return 2;
+    }
     if (!tma_chained) threshold_signhash_kernel<<<items_grid, 1024, sm_thr, stream>>>(a);
     if (rec && a.item_done) {
         const size_t sm_rec = 4 * sizeof(int32_t) * (size_t)a.k;
@@ -569,6 +593,7 @@ void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const Reconci
     } else {
         compact_kernel<uint16_t><<<a.grid, kScoreThreads, 0, stream>>>(a);
     }
+    return tma_chained ? 2 : 3;
 }
 
 void launch_select_exact(const SelArgs& a, cudaStream_t stream) {

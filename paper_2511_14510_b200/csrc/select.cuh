@@ -55,7 +55,8 @@ struct SelArgs {
 struct ReconcileArgs;
 // rec: offloaded heads in a decode step — the compaction kernel also reconciles
 // their entries (needs a.item_done); null: compaction only
-void launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec = nullptr);
+// Returns the number of kernels launched.
+int launch_select_signhash(const SelArgs& a, cudaStream_t stream, const ReconcileArgs* rec = nullptr);
 void launch_select_exact(const SelArgs& a, cudaStream_t stream);
 // Query sign bits for op-level calls (one CTA): q64 [m][d] -> qbits [m][words].
 void launch_hash_queries(const double* q64, int m, int d, const double* proj_t, int bits,

@@ -201,19 +201,15 @@ __device__ __forceinline__ double key_score<uint64_t>(uint64_t k) { return key_t
 // One (item, chunk) unit, kScoreThreads threads; s_gt/s_eq = kScoreThreads/32
 // ints each. Ends with __syncthreads() (when the chunk exists).
 template <typename KeyT>
-__device__ __forceinline__ void compact_unit(const SelArgs& a, int item, int chunk, int* s_gt, int* s_eq) {
+__device__ __forceinline__ void compact_body(const SelArgs& a, const SelItem& it, int item, int chunk, KeyT T, int take,
+                                             int base, int* s_gt, int* s_eq) {
     constexpr int kW = kScoreThreads / 32;
     constexpr int kRowsPerWarp = kScoreChunk / kW;  // 512
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     {
-        const SelItem it = a.items[item];
         const int start = chunk * kScoreChunk;
-        if (start >= it.n) return;
         const int end = min(start + kScoreChunk, it.n);
-        const KeyT T = (KeyT)a.thresh[item];
-        const int take = a.chunk_take[(size_t)item * a.max_chunks + chunk];
-        const int base = a.chunk_base[(size_t)item * a.max_chunks + chunk];
         const KeyT* keys = (sizeof(KeyT) == 2 ? (const KeyT*)(a.key16 + (size_t)item * a.nmax)
                                               : (const KeyT*)(a.key64 + (size_t)item * a.nmax));
         const int w0 = start + warp * kRowsPerWarp, w1 = min(w0 + kRowsPerWarp, end);
@@ -256,6 +252,70 @@ __device__ __forceinline__ void compact_unit(const SelArgs& a, int item, int chu
         }
         __syncthreads();
     }
+}
+
+template <typename KeyT>
+__device__ __forceinline__ void compact_unit(const SelArgs& a, int item, int chunk, int* s_gt, int* s_eq) {
+    const SelItem it = a.items[item];
+    if (chunk * kScoreChunk >= it.n) return;
+    compact_body<KeyT>(a, it, item, chunk, (KeyT)a.thresh[item], a.chunk_take[(size_t)item * a.max_chunks + chunk],
+                       a.chunk_base[(size_t)item * a.max_chunks + chunk], s_gt, s_eq);
+}
+
+// Max bins of the fused quota (hash_bits <= 512).
+constexpr int kMaxBins = 64 * kMaxHashWords + 1;
+
+// threshold_item's result for ONE chunk, recomputed by that chunk's compaction
+// CTA from the item's chunk histograms (sign-hash decode, items of <= 64
+// chunks): one pass keeps, per bin, the item total, the sum over the chunks
+// before this one and this chunk's own count. Then T = the k-th largest S,
+// gt_before = sum over bins > T of the earlier chunks' counts, eq_before = the
+// earlier chunks' ties; the greedy tie quotas of the earlier chunks sum to
+// min(eq_before, need), so
+//   base = gt_before + min(eq_before, need),
+//   take = max(0, min(this chunk's ties, need - eq_before)),
+// exactly the values threshold_item writes. Every CTA of an item derives the
+// same T from the same counts: no cross-CTA handoff, and no separate
+// threshold launch (one kernel boundary less in front of each gather: in the
+// step graph a boundary waits for the host reads the running gather has
+// queued, profiles/r2/README.md).
+__device__ __forceinline__ void chunk_quota(const SelArgs& a, int item, int chunk, int nch, uint32_t* tot,
+                                            uint32_t* pre, uint32_t* cur, int* sts, int* red, int& T, int& take,
+                                            int& base) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t* hist = a.chunk_hist + (size_t)item * a.max_chunks * a.nb;
+    for (int b = threadIdx.x; b < a.nb; b += blockDim.x) {
+        uint32_t s = 0, p = 0, x = 0;
+#pragma unroll 8
+        for (int c = 0; c < nch; ++c) {
+            const uint32_t h = __ldcg(hist + (size_t)c * a.nb + b);
+            if (c == chunk) {
+                p = s;
+                x = h;
+            }
+            s += h;
+        }
+        tot[b] = s;
+        pre[b] = p;
+        cur[b] = x;
+    }
+    __syncthreads();
+    if (warp == 0) threshold_walk(a, tot, sts);
+    __syncthreads();
+    T = sts[0];
+    const int need = a.k - sts[1];
+    int g = 0;
+    for (int b = threadIdx.x; b < a.nb; b += blockDim.x) g += b > T ? (int)pre[b] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+    if (lane == 0) red[warp] = g;
+    __syncthreads();
+    int gt_before = 0;
+    for (int w = 0; w < nwarps; ++w) gt_before += red[w];
+    const int eq_before = T >= 0 ? (int)pre[T] : 0, mine = T >= 0 ? (int)cur[T] : 0;
+    base = gt_before + min(eq_before, need);
+    take = max(0, min(mine, need - eq_before));
+    __syncthreads();  // tot/pre/cur/red are reused by the next unit
 }
 
 
