@@ -10,7 +10,7 @@ for c in 1 3 4; do
 done
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 1100 -c 765 --csv \
   --log-file gpurun_out/ev2_launches.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-for k in attn_mma_stream score_signhash threshold_signhash; do
+for k in attn_mma_stream score_signhash compact_quota gather_engine_tma; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 200 -c 1 \
     -o /tmp/ev2_$k -f python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
   ncu -i /tmp/ev2_$k.ncu-rep --page details --csv > gpurun_out/ev2_ncu_${k}_details.csv 2>&1
