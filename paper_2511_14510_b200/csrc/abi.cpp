@@ -760,9 +760,9 @@ clo_status clo_plan_partition(const double* difficulty, int L, int H, double t_c
                               uint64_t persist_bytes_per_head, uint64_t hbm_budget_bytes,
                               int* persistent_out, int* n_p_out, int* n_dropped_out) {
     return guarded([&] {  // head_profile.cpp:80-154
-        if (L <= 0) fail(CLO_ERR_ARGUMENT, "no profiles to partition");
+        if (L <= 0) fail(CLO_ERR_ARGUMENT, "plan_partition: empty head-profile list");
         if (!(t_comp_s > 0.0) || !(pcie_bw > 0.0) || !(mem_head_bytes > 0.0))
-            fail(CLO_ERR_ARGUMENT, "partition cost terms must be positive");
+            fail(CLO_ERR_ARGUMENT, "plan_partition: every cost term must be > 0");
         const int n_p = (int)std::floor(t_comp_s * pcie_bw / mem_head_bytes);
         std::fill(persistent_out, persistent_out + (size_t)L * H, 0);
         for (int l = 0; l < L; ++l) {
@@ -784,7 +784,7 @@ clo_status clo_plan_partition(const double* difficulty, int L, int H, double t_c
         }
         const uint64_t layer0 = (uint64_t)H * persist_bytes_per_head;
         if (hbm_budget_bytes > 0 && layer0 > hbm_budget_bytes)
-            fail(CLO_ERR_CONFIG, "HBM budget cannot hold the mandatory layer-0 heads");
+            fail(CLO_ERR_CONFIG, "plan_partition: the layer-0 heads alone exceed the HBM budget");
         int dropped = 0;
         if (hbm_budget_bytes > 0) {
             for (;;) {
@@ -801,7 +801,7 @@ clo_status clo_plan_partition(const double* difficulty, int L, int H, double t_c
                             dh = h;
                         }
                     }
-                if (dl < 0) fail(CLO_ERR_CONFIG, "HBM budget infeasible even with no optional persistent heads");
+                if (dl < 0) fail(CLO_ERR_CONFIG, "plan_partition: no plan fits the HBM budget, even without optional persistent heads");
                 persistent_out[(size_t)dl * H + dh] = 0;
                 ++dropped;
             }
