@@ -296,7 +296,15 @@ __global__ void __launch_bounds__(kScoreThreads) compact_kernel(SelArgs a) {
 }
 
 // Compaction with the threshold recomputed per CTA (chunk_quota): sign-hash
-// items of <= 64 chunks, one launch instead of threshold + compaction.
+// items of <= quota_max_chunks() chunks, one launch instead of threshold +
+// compaction (each CTA reads its item's nch x nb histogram words from L2).
+int quota_max_chunks() {  // CLO_QUOTA_MAX_CHUNKS (experiment switch), default 64
+    static const int v = [] {
+        const char* e = getenv("CLO_QUOTA_MAX_CHUNKS");
+        return e && atoi(e) > 0 ? atoi(e) : 64;
+    }();
+    return v;
+}
 __global__ void __launch_bounds__(kScoreThreads) compact_quota_kernel(SelArgs a) {
     __shared__ int s_gt[kWarps], s_eq[kWarps], s_sts[2], s_red[kWarps];
     __shared__ uint32_t s_tot[kMaxBins], s_pre[kMaxBins], s_cur[kMaxBins];
@@ -581,7 +589,7 @@ int launch_select_signhash(const SelArgs& a, cudaStream_t stream, const Reconcil
         const char* e = getenv("CLO_COMPACT_QUOTA");
         return !(e && e[0] == '0');
     }();
-    if (quota && !tma_chained && !rec && a.max_chunks <= 64 && a.nb <= kMaxBins) {
+    if (quota && !tma_chained && !rec && a.max_chunks <= quota_max_chunks() && a.nb <= kMaxBins) {
         compact_quota_kernel<<<a.grid, kScoreThreads, 0, stream>>>(a);
         return 2;
     }
