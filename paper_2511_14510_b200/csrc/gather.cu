@@ -734,11 +734,11 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 
 // Copy variant by host-region size (measured, profiles/README.md): with
 // per-head host regions up to 48 MiB (128K rows of 256 B) the TMA bulk copy
-// (1 warp, 1 stage of 32 rows = 8 KiB shared memory, 128 CTAs) wins: its
+// (1 warp, 1 stage of 32 rows = 8 KiB shared memory, 112 CTAs) wins: its
 // CTAs hold no registers for data in flight and co-reside with the attention
 // and selection CTAs (configs[1]: +3.5%; 64K x 32 sequences: +24%). Over larger
 // regions, where each row's host-address translation misses, the LSU copy
-// (48 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
+// (24 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
 // outstanding and wins (512K: +8%, 1M: +20%).
 // CLO_GATHER=lsu|tma forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
 void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stream) {
@@ -807,7 +807,7 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
     const int use = mode == 0 ? (small_region && sm <= 200 * 1024 ? 2 : 1) : mode;
     if (use == 2 && sm <= 200 * 1024) {
         const int64_t groups = (int64_t)a.items_cap * (v.kv_fused ? 1 : 2) * ((v.k + kTmaRows - 1) / kTmaRows);
-        const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : 128;  // measured: 128 one-warp CTAs
+        const int64_t warps = ctas > 0 ? (int64_t)ctas * shape.x : 112;  // measured: 112 one-warp CTAs (104-120 beat 96 and 128)
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(warps, groups) / shape.x);
         cudaFuncSetAttribute(gather_engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
