@@ -738,7 +738,7 @@ void launch_reconcile(const ReconcileArgs& a, cudaStream_t stream) {
 // CTAs hold no registers for data in flight and co-reside with the attention
 // and selection CTAs (configs[1]: +3.5%; 64K x 32 sequences: +24%). Over larger
 // regions, where each row's host-address translation misses, the LSU copy
-// (24 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
+// (48 CTAs x 32 KiB of 16-byte loads in flight) keeps more requests
 // outstanding and wins (512K: +8%, 1M: +20%).
 // CLO_GATHER=lsu|tma forces a variant; CLO_GATHER_TMA_SHAPE="warps,stages".
 void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stream) {
@@ -813,13 +813,15 @@ void launch_gather_engine(const GatherEngineArgs& a, int ctas, cudaStream_t stre
         gather_engine_tma_kernel<<<grid, shape.x * 32, sm, stream>>>(a, shape.y);
         return;
     }
-    // PCIe needs well over 100 KB in flight; 24 CTAs x 32 KiB keep the link
-    // busy over large host regions with a shallower queue of host reads (every
-    // kernel boundary elsewhere waits for that queue): configs[3] 872 / 969
-    // tokens/s vs 864 / 900 with 48 CTAs on two boxes (profiles/r2).
+    // PCIe needs well over 100 KB in flight over large host regions (every
+    // row's host translation misses). 48 CTAs x 32 KiB: on the final tree
+    // (one box, same session) configs[2] 532 / 551 / 567 / 570 tokens/s with
+    // 24 / 40 / 48 / 64 CTAs and configs[3] 781 / 789 / 811 with 24 / 40 / 48;
+    // an earlier tree had favoured 24 at configs[3] (872 / 969 vs 864 / 900 on
+    // two boxes), long contexts vary most between boxes (profiles/r2).
     const int64_t units = v.kv_fused ? (int64_t)a.items_cap * ((v.k * 2 * vpr + kUnitVecs - 1) / kUnitVecs)
                                      : (int64_t)a.items_cap * 2 * ((v.k * vpr + kUnitVecs - 1) / kUnitVecs);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 24, units));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas > 0 ? ctas : 48, units));
     gather_engine_kernel<<<grid, kGatherThreads, 0, stream>>>(a);
 }
 
